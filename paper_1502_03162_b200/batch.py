@@ -1,0 +1,203 @@
+"""Batched entry points the per-call reference seam cannot express.
+
+* :class:`BatchRenderer` -- one source through every (ear, direction) of a
+  model set in one fused launch (BASELINE configs 1-3).  Equivalent to
+  ``Renderer(model_e).render(y, d)`` for all e, d (engine/__init__.py:238-260).
+* :class:`MixRenderer` -- many sources, each at one direction, summed into a
+  stereo (per-ear) mix with the reflection filters applied first and the
+  resonance once on the mix (configs 4 offline and 5).  Equivalent to
+  ``sum_s Renderer(model_e).render(y_s, dir(s))`` by the associativity the
+  paper factorizes for (tests/test_acceptance.py:283-300).
+* :class:`StreamRenderer` -- the same mixdown in fixed-size blocks with
+  carried overlap history (config 4), one kernel launch per block.
+
+All arrays are CUDA tensors; nothing here touches the host except the small
+tap tables at construction.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import DataError
+
+
+def _as_models(models):
+    if isinstance(models, (list, tuple)):
+        ms = list(models)
+    else:
+        ms = [models]
+    if not ms:
+        raise DataError("need at least one model (one per ear)")
+    D = ms[0].num_directions
+    K = ms[0].reflection_length
+    lf = ms[0].resonance_taps.size
+    for m in ms[1:]:
+        if m.num_directions != D or m.reflection_length != K or m.resonance_taps.size != lf:
+            raise DataError("all ears must share directions, reflection length and resonance length")
+    return ms, D, K, lf
+
+
+def model_rows(models):
+    """Ear-major (indices, values) pairs; dense rows drop zeros as sparse_parts does (engine/__init__.py:148-152)."""
+    rows = []
+    for m in models:
+        for d in range(m.num_directions):
+            if m.is_sparse:
+                sf = m.reflections[d]
+                if sf.length != m.reflection_length:
+                    raise DataError("all reflection filters of a model must share one length")
+                rows.append((np.asarray(sf.indices, np.int64), np.asarray(sf.values, np.float64)))
+            else:
+                dense = m.reflection(d)
+                idx = np.flatnonzero(dense).astype(np.int64)
+                rows.append((idx, dense[idx]))
+    return rows
+
+
+class _ModelSet:
+    def __init__(self, models):
+        self.models, self.dirs, self.K, self.lf = _as_models(models)
+        self.ears = len(self.models)
+        f = np.stack([np.asarray(m.resonance_taps, np.float64) for m in self.models])
+        if not np.all(np.isfinite(f)):
+            raise DataError("taps contain non-finite values")
+        self.rows = model_rows(self.models)
+        self.row_nnz = np.array([r[0].size for r in self.rows], dtype=np.int64)
+        self.taps = _lib.Taps(self.rows, self.K)
+        self.native = _lib.NativeRenderer(f, self.taps, self.dirs)
+        self.M = self.lf + self.K - 1
+
+
+class BatchRenderer(_ModelSet):
+    """y -> out[e, d, :] = (y * f_e) * g_{e,d} for every ear and direction, fused.
+
+    ``counters`` follows Renderer.counters: the resonance stage is counted once
+    per ear and call, the reflection stage per (ear, direction).
+    """
+
+    def __init__(self, models):
+        super().__init__(models)
+        self.counters = {"resonance_macs": 0, "reflection_macs": 0, "calls": 0}
+
+    def out_len(self, ny: int) -> int:
+        return ny + self.M - 1
+
+    def alloc(self, ny: int):
+        """Output buffer [ears, dirs, pitch] (pitch >= out_len, 16-byte rows)."""
+        t = _lib.require_cuda()
+        pitch = self.native.min_pitch(ny)
+        return t.empty((self.ears, self.dirs, pitch), device="cuda", dtype=t.float32)
+
+    def render_all(self, y, out=None, stream=None, check_finite: bool = True):
+        """Returns a [ears, dirs, out_len] float32 view (of ``out`` when given)."""
+        t = _lib.require_cuda()
+        if isinstance(y, t.Tensor):
+            x = y.to(device="cuda", dtype=t.float32).contiguous()
+        else:
+            x = t.from_numpy(np.ascontiguousarray(getattr(y, "samples", y), dtype=np.float32)).to("cuda")
+        if x.ndim != 1 or x.numel() == 0:
+            raise DataError("signal must be a non-empty 1-d array")
+        if check_finite and not bool(t.isfinite(x).all()):
+            raise DataError("signal contains non-finite samples")
+        ny = x.numel()
+        if out is None:
+            out = self.alloc(ny)
+        if out.dtype != t.float32 or not out.is_cuda or out.dim() != 3 or out.shape[:2] != (self.ears, self.dirs):
+            raise DataError("output must be a float32 CUDA tensor of shape [ears, dirs, pitch]")
+        if out.stride(2) != 1 or out.stride(1) != out.shape[2] or out.stride(0) != out.shape[1] * out.shape[2]:
+            raise DataError("output must be contiguous")
+        pitch = out.shape[2]
+        if pitch < self.out_len(ny):
+            raise DataError("output pitch %d < %d samples" % (pitch, self.out_len(ny)))
+        self.native.render(x, out, pitch, stream)
+        self.counters["resonance_macs"] += self.ears * self.lf * ny
+        self.counters["reflection_macs"] += int(self.row_nnz.sum()) * (ny + self.lf - 1)
+        self.counters["calls"] += 1
+        return out[:, :, : self.out_len(ny)]
+
+    def reflect(self, yf, ear: int, out=None, stream=None):
+        """Stage 2 only for one ear: rows (yf * g_{ear,d}) for all d; yf = y*f_ear on the device."""
+        t = _lib.require_cuda()
+        x = yf.to(device="cuda", dtype=t.float32).contiguous()
+        L = x.numel() + self.K - 1
+        if out is None:
+            out = t.empty((self.dirs, (L + 3) // 4 * 4), device="cuda", dtype=t.float32)
+        self.native.reflect(ear, x, out, out.shape[1], stream)
+        self.counters["reflection_macs"] += int(self.row_nnz[ear * self.dirs:(ear + 1) * self.dirs].sum()) * x.numel()
+        return out[:, :L]
+
+
+class MixRenderer(_ModelSet):
+    """S sources at directions src_dir -> per-ear mix  out[e] = sum_s (y_s * f_e) * g_{e,dir(s)}.
+
+    Computed as  out[e] = f_e * z[e],  z[e] = sum_s y_s * g_{e,dir(s)}  (reflection first).
+    """
+
+    def __init__(self, models, src_dir, T: int):
+        super().__init__(models)
+        self.src_dir = np.ascontiguousarray(src_dir, dtype=np.int32)
+        if self.src_dir.ndim != 1 or self.src_dir.size == 0:
+            raise DataError("need at least one source")
+        if np.any(self.src_dir < 0) or np.any(self.src_dir >= self.dirs):
+            bad = int(self.src_dir[(self.src_dir < 0) | (self.src_dir >= self.dirs)][0])
+            raise DataError("direction %d out of range" % bad)
+        self.S = self.src_dir.size
+        self.T = int(T)
+        self.mixer = _lib.NativeMixer(self.native, self.src_dir, self.T)
+        self.z_len = self.mixer.z_len()
+        self.out_len = self.mixer.out_len()
+
+    def alloc_z(self):
+        t = _lib.require_cuda()
+        return t.zeros((self.ears, (self.z_len + 3) // 4 * 4), device="cuda", dtype=t.float32)
+
+    def partial(self, y, s0: int = 0, count: int | None = None, z=None, stream=None):
+        """z[e] = sum over sources [s0, s0+count) of y_s * g_{e,dir(s)}; y row i is source s0+i."""
+        t = _lib.require_cuda()
+        count = self.S - s0 if count is None else int(count)
+        if y.dim() != 2 or y.shape[0] < count or y.shape[1] < self.T or y.stride(1) != 1:
+            raise DataError("sources must be a [count, >=T] row-major CUDA tensor")
+        if y.dtype != t.float32 or not y.is_cuda:
+            raise DataError("sources must be float32 CUDA tensors")
+        if z is None:
+            z = self.alloc_z()
+        self.mixer.partial(y, y.stride(0), s0, count, z, z.stride(0), stream)
+        return z
+
+    def finish(self, z, out=None, stream=None):
+        t = _lib.require_cuda()
+        if out is None:
+            out = t.empty((self.ears, (self.out_len + 3) // 4 * 4), device="cuda", dtype=t.float32)
+        self.mixer.finish(z, z.stride(0), out, out.stride(0), stream)
+        return out[:, : self.out_len]
+
+    def render(self, y, stream=None):
+        return self.finish(self.partial(y, stream=stream), stream=stream)
+
+
+class StreamRenderer(_ModelSet):
+    """Block-by-block mixdown with carried history: step n returns samples
+    [n*B, (n+1)*B) of :class:`MixRenderer`'s output for the concatenated input."""
+
+    def __init__(self, models, src_dir, block: int):
+        super().__init__(models)
+        self.src_dir = np.ascontiguousarray(src_dir, dtype=np.int32)
+        if np.any(self.src_dir < 0) or np.any(self.src_dir >= self.dirs):
+            raise DataError("direction out of range")
+        self.S = self.src_dir.size
+        self.B = int(block)
+        self.streamer = _lib.NativeStreamer(self.native, self.src_dir, self.B)
+
+    def reset(self, stream=None):
+        self.streamer.reset(stream)
+
+    def step(self, block, out=None, stream=None):
+        t = _lib.require_cuda()
+        if block.shape != (self.S, self.B) or block.dtype != t.float32 or not block.is_cuda:
+            raise DataError("block must be a float32 CUDA tensor of shape [S, B]")
+        block = block.contiguous()
+        if out is None:
+            out = t.empty((self.ears, self.B), device="cuda", dtype=t.float32)
+        self.streamer.step(block, out, stream)
+        return out

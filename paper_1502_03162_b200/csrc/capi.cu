@@ -1,0 +1,657 @@
+// C ABI implementation (include/toep_b200.h).  Validation mirrors the
+// reference's DataError rules; kernels live in render.cu / fir_mix.cu.
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/toep_b200.h"
+#include "launch.h"
+
+using namespace toep;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? TOEP_ERR_NOMEM : TOEP_ERR_CUDA, "%s: %s", where,
+              cudaGetErrorString(e));
+}
+#define TOEP_CUDA(call)                                     \
+  do {                                                      \
+    cudaError_t _e = (call);                                \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);     \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count_cached() {
+  static thread_local int dev = -1, count = 0;
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return 148;
+  if (d != dev) {
+    dev = d;
+    if (cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) count = 148;
+  }
+  return count;
+}
+
+inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// ------------------------------------------------------------ tap tables ----
+struct toep_taps {
+  int rows = 0, length = 0, max_nnz = 0, kwin = -1, tap_stride = 1, uniform = 0;
+  long long total = 0;
+  int2* d_kw = nullptr;   // col = kwin - offset (TMEM kernels)
+  int2* d_raw = nullptr;  // col = offset (generic / streaming kernels)
+  int* d_nnz = nullptr;
+  bool stream_owned = false;  // freed with cudaFreeAsync on `owner`
+  cudaStream_t owner = nullptr;
+};
+
+static bool uniform_supported(int n) { return n == 4 || n == 8 || n == 12 || n == 16 || n == 24 || n == 32; }
+
+static int taps_build(int32_t rows, int32_t length, const int64_t* row_ptr, const int64_t* indices,
+                      const float* values, bool stream_owned, cudaStream_t st, toep_taps** out) {
+  if (!out) return fail(TOEP_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (rows < 1) return fail(TOEP_ERR_INVALID, "need at least one filter row, got %d", rows);
+  if (length < 1) return fail(TOEP_ERR_INVALID, "filter length must be at least 1");  // sparsify.py:87-88
+  if (!row_ptr) return fail(TOEP_ERR_INVALID, "null row_ptr");
+  if (row_ptr[0] != 0) return fail(TOEP_ERR_INVALID, "row_ptr[0] must be 0");
+  int max_nnz = 0;
+  bool uni = true;
+  for (int r = 0; r < rows; ++r) {
+    const long long a = row_ptr[r], b = row_ptr[r + 1];
+    if (b < a) return fail(TOEP_ERR_INVALID, "row_ptr must be non-decreasing (row %d)", r);
+    const long long n = b - a;
+    if (n > length) return fail(TOEP_ERR_INVALID, "row %d has %lld taps for length %d", r, n, length);
+    for (long long k = a; k < b; ++k) {
+      const long long o = indices[k];
+      if (o < 0 || o >= length)  // sparsify.py:83-84
+        return fail(TOEP_ERR_INVALID, "indices must lie in [0, %d) (row %d)", length, r);
+      if (k > a && o <= indices[k - 1])  // sparsify.py:81-82
+        return fail(TOEP_ERR_INVALID, "indices must be strictly increasing (row %d)", r);
+      if (!std::isfinite(values[k])) return fail(TOEP_ERR_INVALID, "values must be finite (row %d)", r);
+    }
+    if (r > 0 && n != max_nnz) uni = false;
+    max_nnz = std::max<int>(max_nnz, (int)n);
+  }
+  auto* t = new (std::nothrow) toep_taps();
+  if (!t) return fail(TOEP_ERR_NOMEM, "host allocation failed");
+  t->rows = rows;
+  t->length = length;
+  t->max_nnz = max_nnz;
+  t->total = row_ptr[rows];
+  t->kwin = render_kwin_for(length);
+  t->tap_stride = std::max(1, max_nnz);
+  t->uniform = (uni && uniform_supported(max_nnz)) ? 1 : 0;
+  t->stream_owned = stream_owned;
+  t->owner = st;
+  const size_t n = (size_t)rows * t->tap_stride;
+  std::vector<int2> kw(n), raw(n);
+  std::vector<int> nnz(rows);
+  for (int r = 0; r < rows; ++r) {
+    const long long a = row_ptr[r], b = row_ptr[r + 1];
+    nnz[r] = (int)(b - a);
+    for (int k = 0; k < t->tap_stride; ++k) {
+      int o = 0;
+      float v = 0.f;
+      if (a + k < b) {
+        o = (int)indices[a + k];
+        v = values[a + k];
+      }
+      int vb;
+      memcpy(&vb, &v, 4);
+      raw[(size_t)r * t->tap_stride + k] = make_int2(o, vb);
+      kw[(size_t)r * t->tap_stride + k] = make_int2(t->kwin > 0 ? t->kwin - o : 0, vb);
+    }
+  }
+  cudaError_t e;
+  if (stream_owned) {
+    e = cudaMallocAsync(&t->d_kw, n * sizeof(int2), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&t->d_raw, n * sizeof(int2), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&t->d_nnz, rows * sizeof(int), st);
+  } else {
+    e = cudaMalloc(&t->d_kw, n * sizeof(int2));
+    if (e == cudaSuccess) e = cudaMalloc(&t->d_raw, n * sizeof(int2));
+    if (e == cudaSuccess) e = cudaMalloc(&t->d_nnz, rows * sizeof(int));
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->d_kw, kw.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->d_raw, raw.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->d_nnz, nnz.data(), rows * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !stream_owned) e = cudaStreamSynchronize(st);  // host staging vectors die here
+  if (e != cudaSuccess) {
+    toep_taps_destroy(t);
+    return cuda_fail(e, "toep_taps_create");
+  }
+  *out = t;
+  return TOEP_OK;
+}
+
+extern "C" {
+
+const char* toep_last_error(void) { return g_err; }
+int toep_abi_version(void) { return TOEP_ABI_VERSION; }
+int toep_sm_count(int* out) {
+  if (!out) return fail(TOEP_ERR_INVALID, "null output");
+  int d = 0;
+  TOEP_CUDA(cudaGetDevice(&d));
+  TOEP_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, d));
+  return TOEP_OK;
+}
+
+int toep_taps_create(int32_t rows, int32_t length, const int64_t* row_ptr, const int64_t* indices,
+                     const float* values, toep_taps** out) {
+  return taps_build(rows, length, row_ptr, indices, values, false, nullptr, out);
+}
+
+int toep_taps_destroy(toep_taps* t) {
+  if (!t) return TOEP_OK;
+  if (t->stream_owned) {
+    if (t->d_kw) cudaFreeAsync(t->d_kw, t->owner);
+    if (t->d_raw) cudaFreeAsync(t->d_raw, t->owner);
+    if (t->d_nnz) cudaFreeAsync(t->d_nnz, t->owner);
+  } else {
+    if (t->d_kw) cudaFree(t->d_kw);
+    if (t->d_raw) cudaFree(t->d_raw);
+    if (t->d_nnz) cudaFree(t->d_nnz);
+  }
+  delete t;
+  return TOEP_OK;
+}
+
+int toep_taps_info(const toep_taps* t, int32_t* rows, int32_t* length, int32_t* max_nnz, int64_t* total_nnz) {
+  if (!t) return fail(TOEP_ERR_INVALID, "null table");
+  if (rows) *rows = t->rows;
+  if (length) *length = t->length;
+  if (max_nnz) *max_nnz = t->max_nnz;
+  if (total_nnz) *total_nnz = t->total;
+  return TOEP_OK;
+}
+
+}  // extern "C"
+
+// Stage-2 ("reflection") launch over `nrows` consecutive rows of a table,
+// all reading the same input signal x (nx samples).
+static int reflect_rows(const toep_taps* t, int row0, int nrows, const float* x, long long nx, float* out,
+                        long long out_pitch, cudaStream_t st) {
+  const long long out_len = nx + t->length - 1;
+  if (t->kwin > 0) {
+    if (!aligned16(out) || (nrows > 1 && out_pitch % 4 != 0))
+      return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");
+    RenderArgs a{};
+    a.x = x;
+    a.nx = nx;
+    a.x_pitch = 0;
+    a.f = nullptr;
+    a.lf_pad = 0;
+    a.taps = t->d_kw + (size_t)row0 * t->tap_stride;
+    a.row_nnz = t->d_nnz + row0;
+    a.tap_stride = t->tap_stride;
+    a.uniform_nnz = t->uniform;
+    a.tap_stride_nnz = t->tap_stride;
+    a.dirs = nrows;
+    a.ears = 1;
+    const int budget_taps = 2048;  // int2 entries staged per group (16 KB)
+    a.dirs_per_group = std::max(1, std::min(nrows, budget_taps / t->tap_stride));
+    a.groups = (nrows + a.dirs_per_group - 1) / a.dirs_per_group;
+    a.n_tiles = (int)((out_len + kW - 1) / kW);
+    a.n_items = (long long)a.groups * a.n_tiles;
+    a.out = out;
+    a.out_pitch = out_pitch;
+    a.out_len = out_len;
+    cudaError_t e = launch_render(a, t->kwin, false, sm_count_cached(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_render(stage 2)");
+    return TOEP_OK;
+  }
+  SparseGenericArgs g{};
+  g.x = x;
+  g.nx = nx;
+  g.x_pitch = 0;
+  g.rows_per_x = 1;
+  g.taps = t->d_raw + (size_t)row0 * t->tap_stride;
+  g.row_nnz = t->d_nnz + row0;
+  g.tap_stride = t->tap_stride;
+  g.rows = nrows;
+  g.out = out;
+  g.out_len = out_len;
+  g.out_pitch = out_pitch;
+  cudaError_t e = launch_sparse_generic(g, st);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_sparse_generic");
+  return TOEP_OK;
+}
+
+static int dense_fir(const float* x, long long nx, long long x_pitch, const float* h_pad, int nh_pad, int h_pitch,
+                     int channels, float* out, long long out_len, long long out_pitch, cudaStream_t st) {
+  FirArgs a{};
+  a.x = x;
+  a.nx = nx;
+  a.x_pitch = x_pitch;
+  a.h = h_pad;
+  a.nh_pad = nh_pad;
+  a.h_pitch = h_pitch;
+  a.out = out;
+  a.out_len = out_len;
+  a.out_pitch = out_pitch;
+  a.channels = channels;
+  cudaError_t e = launch_fir(a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_fir");
+  return TOEP_OK;
+}
+
+extern "C" {
+
+int toep_taps_conv(const toep_taps* t, int32_t row, const float* y, int64_t ny, float* out, void* stream) {
+  if (!t) return fail(TOEP_ERR_INVALID, "null table");
+  if (row < 0 || row >= t->rows) return fail(TOEP_ERR_INVALID, "row %d out of range", row);
+  if (ny < 1 || !y || !out) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  return reflect_rows(t, row, 1, y, ny, out, 0, S(stream));
+}
+
+int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps, float* out, int64_t* macs,
+                    void* stream) {
+  if (ny < 1 || !y) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  if (ntaps < 1 || !taps) return fail(TOEP_ERR_INVALID, "taps must be a non-empty 1-d array");
+  if (!out) return fail(TOEP_ERR_INVALID, "null output");
+  cudaStream_t st = S(stream);
+  const long long nh_pad = round_up(ntaps, 16);
+  if (nh_pad > (1LL << 30)) return fail(TOEP_ERR_UNSUPPORTED, "too many taps");
+  float* h = nullptr;
+  TOEP_CUDA(cudaMallocAsync(&h, nh_pad * sizeof(float), st));
+  cudaError_t e = cudaMemsetAsync(h, 0, nh_pad * sizeof(float), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, taps, ntaps * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  int rc = (e == cudaSuccess) ? dense_fir(y, ny, 0, h, (int)nh_pad, 0, 1, out, ny + ntaps - 1, 0, st)
+                              : cuda_fail(e, "toep_conv_dense staging");
+  cudaFreeAsync(h, st);
+  if (rc == TOEP_OK && macs) *macs = (int64_t)ntaps * ny;  // _kernels.pyx:24
+  return rc;
+}
+
+int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const float* values, int64_t nnz,
+                     int64_t length, float* out, int64_t* macs, void* stream) {
+  if (ny < 1 || !y) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  if (length < 1 || length > (1LL << 30)) return fail(TOEP_ERR_INVALID, "bad filter length");
+  if (nnz < 0 || (nnz > 0 && (!indices || !values))) return fail(TOEP_ERR_INVALID, "bad tap arrays");
+  cudaStream_t st = S(stream);
+  const int64_t row_ptr[2] = {0, nnz};
+  toep_taps* t = nullptr;
+  int rc = taps_build(1, (int32_t)length, row_ptr, indices, values, true, st, &t);
+  if (rc != TOEP_OK) return rc;
+  rc = reflect_rows(t, 0, 1, y, ny, out, 0, st);
+  toep_taps_destroy(t);
+  if (rc == TOEP_OK && macs) *macs = nnz * ny;  // _kernels.pyx:43
+  return rc;
+}
+
+}  // extern "C"
+
+// -------------------------------------------------------------- renderer ----
+struct toep_renderer {
+  int ears = 0, lf = 0, lf_pad = 0, dirs = 0;
+  const toep_taps* g = nullptr;
+  float* d_f = nullptr;  // [ears][lf_pad]
+};
+
+static int render_dirs_per_group(const toep_renderer* r) {
+  // keep the CTA's shared memory inside its 1/(512/COLS) share of the SM
+  const int kwin = r->g->kwin;
+  const int per_sm = 512 / (kR + kwin);
+  const int budget = 227 * 1024 / per_sm - 1024;
+  int dpg = std::min(r->dirs, std::max(1, 4096 / r->g->tap_stride));
+  while (dpg > 1 && (int)render_smem_bytes(kwin, true, r->lf_pad, dpg, r->g->tap_stride) > budget) dpg = (dpg + 1) / 2;
+  return dpg;
+}
+
+extern "C" {
+
+int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const toep_taps* g, int32_t dirs,
+                         toep_renderer** out) {
+  if (!out) return fail(TOEP_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (ears < 1) return fail(TOEP_ERR_INVALID, "need at least one ear");
+  if (lf < 1 || !f_host) return fail(TOEP_ERR_INVALID, "resonance taps must be a non-empty 1-d array");
+  if (!g) return fail(TOEP_ERR_INVALID, "null reflection table");
+  if (dirs < 1 || (long long)dirs * ears != g->rows)
+    return fail(TOEP_ERR_INVALID, "table has %d rows, expected ears*dirs = %lld", g->rows, (long long)dirs * ears);
+  for (long long i = 0; i < (long long)ears * lf; ++i)
+    if (!std::isfinite(f_host[i])) return fail(TOEP_ERR_INVALID, "taps contain non-finite values");
+  auto* r = new (std::nothrow) toep_renderer();
+  if (!r) return fail(TOEP_ERR_NOMEM, "host allocation failed");
+  r->ears = ears;
+  r->lf = lf;
+  r->lf_pad = (int)round_up(lf, 16);
+  r->dirs = dirs;
+  r->g = g;
+  std::vector<float> fp((size_t)ears * r->lf_pad, 0.f);
+  for (int e = 0; e < ears; ++e)
+    for (int j = 0; j < lf; ++j) fp[(size_t)e * r->lf_pad + j] = f_host[(size_t)e * lf + j];
+  cudaError_t e = cudaMalloc(&r->d_f, fp.size() * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpy(r->d_f, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    toep_renderer_destroy(r);
+    return cuda_fail(e, "toep_renderer_create");
+  }
+  *out = r;
+  return TOEP_OK;
+}
+
+int toep_renderer_destroy(toep_renderer* r) {
+  if (!r) return TOEP_OK;
+  if (r->d_f) cudaFree(r->d_f);
+  delete r;
+  return TOEP_OK;
+}
+
+int64_t toep_renderer_out_len(const toep_renderer* r, int64_t ny) {
+  return r ? ny + r->lf + r->g->length - 2 : -1;
+}
+int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny) {
+  return r ? round_up(toep_renderer_out_len(r, ny), 4) : -1;
+}
+
+int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, float* out, int64_t out_pitch,
+                         void* stream) {
+  if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
+  if (ny < 1 || !y) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  if (!out) return fail(TOEP_ERR_INVALID, "null output");
+  const long long out_len = toep_renderer_out_len(r, ny);
+  const long long rows = (long long)r->ears * r->dirs;
+  if (rows > 1 && out_pitch < out_len) return fail(TOEP_ERR_INVALID, "output pitch %lld < %lld", (long long)out_pitch, out_len);
+  cudaStream_t st = S(stream);
+  const toep_taps* g = r->g;
+  if (g->kwin > 0) {
+    if (!aligned16(out) || (rows > 1 && out_pitch % 4 != 0))
+      return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");
+    RenderArgs a{};
+    a.x = y;
+    a.nx = ny;
+    a.f = r->d_f;
+    a.lf_pad = r->lf_pad;
+    a.taps = g->d_kw;
+    a.row_nnz = g->d_nnz;
+    a.tap_stride = g->tap_stride;
+    a.uniform_nnz = g->uniform;
+    a.tap_stride_nnz = g->tap_stride;
+    a.dirs = r->dirs;
+    a.ears = r->ears;
+    a.dirs_per_group = render_dirs_per_group(r);
+    a.groups = (r->dirs + a.dirs_per_group - 1) / a.dirs_per_group;
+    a.n_tiles = (int)((out_len + kW - 1) / kW);
+    a.n_items = (long long)a.ears * a.groups * a.n_tiles;
+    a.out = out;
+    a.out_pitch = out_pitch;
+    a.out_len = out_len;
+    cudaError_t e = launch_render(a, g->kwin, true, sm_count_cached(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_render");
+    return TOEP_OK;
+  }
+  // long reflection filters: y*f per ear into scratch, then the banded kernel
+  const long long nyf = ny + r->lf - 1;
+  const long long pitch = round_up(nyf, 4);
+  float* yf = nullptr;
+  TOEP_CUDA(cudaMallocAsync(&yf, (size_t)pitch * r->ears * sizeof(float), st));
+  int rc = TOEP_OK;
+  for (int e = 0; e < r->ears && rc == TOEP_OK; ++e)
+    rc = dense_fir(y, ny, 0, r->d_f + (size_t)e * r->lf_pad, r->lf_pad, 0, 1, yf + e * pitch, nyf, 0, st);
+  if (rc == TOEP_OK) {
+    SparseGenericArgs ga{};
+    ga.x = yf;
+    ga.nx = nyf;
+    ga.x_pitch = pitch;
+    ga.rows_per_x = r->dirs;
+    ga.taps = g->d_raw;
+    ga.row_nnz = g->d_nnz;
+    ga.tap_stride = g->tap_stride;
+    ga.rows = (int)rows;
+    ga.out = out;
+    ga.out_len = out_len;
+    ga.out_pitch = out_pitch;
+    cudaError_t e = launch_sparse_generic(ga, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "launch_sparse_generic");
+  }
+  cudaFreeAsync(yf, st);
+  return rc;
+}
+
+int toep_renderer_reflect(const toep_renderer* r, int32_t ear, const float* yf, int64_t nyf, float* out,
+                          int64_t out_pitch, void* stream) {
+  if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
+  if (ear < 0 || ear >= r->ears) return fail(TOEP_ERR_INVALID, "ear %d out of range", ear);
+  if (nyf < 1 || !yf || !out) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  if (r->dirs > 1 && out_pitch < nyf + r->g->length - 1) return fail(TOEP_ERR_INVALID, "output pitch too small");
+  return reflect_rows(r->g, ear * r->dirs, r->dirs, yf, nyf, out, out_pitch, S(stream));
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------- mixer ----
+struct toep_mixer {
+  const toep_renderer* r = nullptr;
+  int S = 0;
+  long long T = 0, zlen = 0;
+  int* d_dir = nullptr;
+  float* d_part = nullptr;
+  size_t part_bytes = 0;
+};
+
+static constexpr int kSrcPerGroup = 256;
+
+extern "C" {
+
+int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32_t n_src, int64_t T,
+                      toep_mixer** out) {
+  if (!out) return fail(TOEP_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
+  if (n_src < 1 || !src_dir_host) return fail(TOEP_ERR_INVALID, "need at least one source");
+  if (T < 1) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  if (r->g->kwin <= 0) return fail(TOEP_ERR_UNSUPPORTED, "mixdown supports reflection length <= 497");
+  if (r->ears > 2) return fail(TOEP_ERR_UNSUPPORTED, "mixdown supports at most 2 ears");
+  for (int s = 0; s < n_src; ++s)
+    if (src_dir_host[s] < 0 || src_dir_host[s] >= r->dirs)  // engine/__init__.py:240-241
+      return fail(TOEP_ERR_INVALID, "direction %d out of range", src_dir_host[s]);
+  auto* m = new (std::nothrow) toep_mixer();
+  if (!m) return fail(TOEP_ERR_NOMEM, "host allocation failed");
+  m->r = r;
+  m->S = n_src;
+  m->T = T;
+  m->zlen = T + r->g->length - 1;
+  cudaError_t e = cudaMalloc(&m->d_dir, n_src * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(m->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    toep_mixer_destroy(m);
+    return cuda_fail(e, "toep_mixer_create");
+  }
+  *out = m;
+  return TOEP_OK;
+}
+
+int toep_mixer_destroy(toep_mixer* m) {
+  if (!m) return TOEP_OK;
+  if (m->d_dir) cudaFree(m->d_dir);
+  if (m->d_part) cudaFree(m->d_part);
+  delete m;
+  return TOEP_OK;
+}
+
+int64_t toep_mixer_z_len(const toep_mixer* m) { return m ? m->zlen : -1; }
+int64_t toep_mixer_out_len(const toep_mixer* m) { return m ? m->zlen + m->r->lf - 1 : -1; }
+
+int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s0, int32_t count, float* z,
+                       int64_t z_pitch, void* stream) {
+  if (!m) return fail(TOEP_ERR_INVALID, "null mixer");
+  if (count < 1 || s0 < 0 || (long long)s0 + count > m->S) return fail(TOEP_ERR_INVALID, "source range out of bounds");
+  if (!y || !z) return fail(TOEP_ERR_INVALID, "null buffer");
+  if (count > 1 && y_pitch < m->T) return fail(TOEP_ERR_INVALID, "source pitch too small");
+  if (m->r->ears > 1 && z_pitch < m->zlen) return fail(TOEP_ERR_INVALID, "z pitch too small");
+  cudaStream_t st = S(stream);
+  const toep_taps* g = m->r->g;
+  const int groups = (count + kSrcPerGroup - 1) / kSrcPerGroup;
+  const int n_tiles = (int)((m->zlen + kW - 1) / kW);
+  const long long part_pitch = (long long)n_tiles * kW;
+  const size_t need = (size_t)groups * m->r->ears * part_pitch * sizeof(float);
+  if (need > m->part_bytes) {
+    if (m->d_part) {
+      TOEP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(m->d_part);
+      m->d_part = nullptr;
+      m->part_bytes = 0;
+    }
+    TOEP_CUDA(cudaMalloc(&m->d_part, need));
+    m->part_bytes = need;
+  }
+  MixArgs a{};
+  a.y = y;
+  a.T = m->T;
+  a.y_pitch = y_pitch;
+  a.src_dir = m->d_dir + s0;
+  a.S = count;
+  a.taps = g->d_kw;
+  a.row_nnz = g->d_nnz;
+  a.tap_stride = g->tap_stride;
+  a.uniform_nnz = g->uniform;
+  a.dirs = m->r->dirs;
+  a.ears = m->r->ears;
+  a.src_per_group = kSrcPerGroup;
+  a.groups = groups;
+  a.n_tiles = n_tiles;
+  a.n_items = (long long)groups * n_tiles;
+  a.part = m->d_part;
+  a.part_pitch = part_pitch;
+  a.zlen = m->zlen;
+  cudaError_t e = launch_mix(a, g->kwin, sm_count_cached(), st);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_mix");
+  e = launch_mix_reduce(m->d_part, groups, m->r->ears, part_pitch, m->zlen, z, z_pitch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_mix_reduce");
+  return TOEP_OK;
+}
+
+int toep_mixer_finish(const toep_mixer* m, const float* z, int64_t z_pitch, float* out, int64_t out_pitch,
+                      void* stream) {
+  if (!m) return fail(TOEP_ERR_INVALID, "null mixer");
+  if (!z || !out) return fail(TOEP_ERR_INVALID, "null buffer");
+  const long long out_len = toep_mixer_out_len(m);
+  if (m->r->ears > 1 && out_pitch < out_len) return fail(TOEP_ERR_INVALID, "output pitch too small");
+  return dense_fir(z, m->zlen, z_pitch, m->r->d_f, m->r->lf_pad, m->r->lf_pad, m->r->ears, out, out_len, out_pitch,
+                   S(stream));
+}
+
+}  // extern "C"
+
+// -------------------------------------------------------------- streamer ----
+struct toep_streamer {
+  const toep_renderer* r = nullptr;
+  int S = 0, B = 0, H = 0, zh = 0, ctas = 0, spc = 0;
+  int* d_dir = nullptr;
+  float* d_yhist = nullptr;
+  float* d_zhist = nullptr;
+  float* d_part = nullptr;
+  unsigned int* d_ticket = nullptr;
+};
+
+extern "C" {
+
+int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, int32_t n_src, int32_t block,
+                         toep_streamer** out) {
+  if (!out) return fail(TOEP_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
+  if (n_src < 1 || !src_dir_host) return fail(TOEP_ERR_INVALID, "need at least one source");
+  if (block < 1 || block > 1024) return fail(TOEP_ERR_UNSUPPORTED, "block size must be in [1, 1024]");
+  if (r->g->length > 4096) return fail(TOEP_ERR_UNSUPPORTED, "streaming supports reflection length <= 4096");
+  for (int s = 0; s < n_src; ++s)
+    if (src_dir_host[s] < 0 || src_dir_host[s] >= r->dirs)
+      return fail(TOEP_ERR_INVALID, "direction %d out of range", src_dir_host[s]);
+  auto* s = new (std::nothrow) toep_streamer();
+  if (!s) return fail(TOEP_ERR_NOMEM, "host allocation failed");
+  s->r = r;
+  s->S = n_src;
+  s->B = block;
+  s->H = (int)round_up(std::max(1, r->g->length - 1), 4);
+  s->zh = r->lf_pad;
+  s->spc = 8;
+  s->ctas = (n_src + s->spc - 1) / s->spc;
+  cudaError_t e = cudaMalloc(&s->d_dir, n_src * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_yhist, (size_t)n_src * s->H * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_zhist, (size_t)r->ears * s->zh * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_part, (size_t)s->ctas * r->ears * block * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_ticket, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(s->d_yhist, 0, (size_t)n_src * s->H * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemset(s->d_zhist, 0, (size_t)r->ears * s->zh * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemset(s->d_ticket, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    toep_streamer_destroy(s);
+    return cuda_fail(e, "toep_streamer_create");
+  }
+  *out = s;
+  return TOEP_OK;
+}
+
+int toep_streamer_destroy(toep_streamer* s) {
+  if (!s) return TOEP_OK;
+  if (s->d_dir) cudaFree(s->d_dir);
+  if (s->d_yhist) cudaFree(s->d_yhist);
+  if (s->d_zhist) cudaFree(s->d_zhist);
+  if (s->d_part) cudaFree(s->d_part);
+  if (s->d_ticket) cudaFree(s->d_ticket);
+  delete s;
+  return TOEP_OK;
+}
+
+int toep_streamer_reset(toep_streamer* s, void* stream) {
+  if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
+  cudaStream_t st = S(stream);
+  TOEP_CUDA(cudaMemsetAsync(s->d_yhist, 0, (size_t)s->S * s->H * sizeof(float), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)s->r->ears * s->zh * sizeof(float), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, sizeof(unsigned int), st));
+  return TOEP_OK;
+}
+
+int toep_streamer_step(toep_streamer* s, const float* block, float* out, void* stream) {
+  if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
+  if (!block || !out) return fail(TOEP_ERR_INVALID, "null buffer");
+  StreamArgs a{};
+  a.block = block;
+  a.B = s->B;
+  a.yhist = s->d_yhist;
+  a.H = s->H;
+  a.src_dir = s->d_dir;
+  a.S = s->S;
+  a.taps = s->r->g->d_raw;
+  a.row_nnz = s->r->g->d_nnz;
+  a.tap_stride = s->r->g->tap_stride;
+  a.dirs = s->r->dirs;
+  a.ears = s->r->ears;
+  a.src_per_cta = s->spc;
+  a.part = s->d_part;
+  a.zhist = s->d_zhist;
+  a.zh = s->zh;
+  a.f = s->r->d_f;
+  a.lf_pad = s->r->lf_pad;
+  a.out = out;
+  a.ctas = s->ctas;
+  a.ticket = s->d_ticket;
+  cudaError_t e = launch_stream_step(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "launch_stream_step");
+  return TOEP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// Device-side building blocks shared by the renderer kernels (sm_100a only).
+//
+//  * TMEM (tensor memory) as a per-lane, dynamically indexable sliding window:
+//    tcgen05.st writes a lane's window row, tcgen05.ld.32x32b.x16 reads 16
+//    consecutive columns starting at a *runtime* column -- this is what lets a
+//    sparse tap list (runtime offsets) feed FFMA without a shared-memory load
+//    per multiply-accumulate.
+//  * cp.async.bulk (TMA, non-tensor) stores from shared memory, so each warp's
+//    output run leaves the SM as one contiguous bulk write.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "launch.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "paper_1502_03162_b200 kernels target sm_100a only"
+#endif
+
+namespace toep {
+
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- TMEM ----
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(unsigned* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(COLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(unsigned base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(float (&d)[16], unsigned ta) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7]),
+        "=f"(d[8]), "=f"(d[9]), "=f"(d[10]), "=f"(d[11]), "=f"(d[12]), "=f"(d[13]), "=f"(d[14]), "=f"(d[15])
+      : "r"(ta)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(unsigned ta, const float (&d)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7]), "f"(d[8]),
+      "f"(d[9]), "f"(d[10]), "f"(d[11]), "f"(d[12]), "f"(d[13]), "f"(d[14]), "f"(d[15])
+      : "memory");
+}
+
+// ------------------------------------------------------- bulk (TMA) ops ----
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(float* gdst, const float* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Padded shared-memory layout for signal tiles read as 16-float chunks by
+// consecutive lanes: 4 pad words per 32 keeps LDS.128 conflict-free.
+__device__ __forceinline__ int padi(int i) { return i + ((i >> 5) << 2); }
+__host__ __device__ constexpr int padded_len(int n) { return n + ((n + 31) / 32) * 4; }
+
+// Register-blocked dense FIR over a padded shared tile:
+//   acc[r] += sum_{j<ntaps} h[j] * x[base + r - j],  r = 0..15
+// `x` is the padded tile, `base` a logical index (multiple of 16) with at
+// least ntaps_padded earlier samples available; `h` is zero-padded to a
+// multiple of 16 in shared memory.  256 FFMA per 8+4 LDS.128.
+__device__ __forceinline__ void fir16_block(float (&acc)[16], const float* __restrict__ x, int base,
+                                            const float* __restrict__ h, int ntaps_padded) {
+  for (int j0 = 0; j0 < ntaps_padded; j0 += 16) {
+    float w[32];
+    const int a = base - j0 - 16;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(&x[padi(a + 4 * q)]);
+      w[4 * q] = v.x;
+      w[4 * q + 1] = v.y;
+      w[4 * q + 2] = v.z;
+      w[4 * q + 3] = v.w;
+    }
+    float hh[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(&h[j0 + 4 * q]);
+      hh[4 * q] = v.x;
+      hh[4 * q + 1] = v.y;
+      hh[4 * q + 2] = v.z;
+      hh[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) acc[r] = fmaf(hh[jj], w[16 + r - jj], acc[r]);
+  }
+}
+
+}  // namespace toep

@@ -1,0 +1,128 @@
+// Internal launcher interface between the C ABI (capi.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace toep {
+
+constexpr int kR = 16;             // outputs per lane (one TMEM x16 load per tap)
+constexpr int kWarps = 4;          // warps per CTA: one per TMEM lane quarter
+constexpr int kThreads = 32 * kWarps;
+constexpr int kW = kThreads * kR;  // outputs per CTA tile (2048)
+
+// Tap tables are row-major "ELL" arrays of int2 {col, value-bits} with
+// col = KWIN - offset (the TMEM window column where the tap's 16-sample
+// slice starts) and a per-row count in row_nnz.  Rows are ear-major:
+// row = ear * dirs + direction.
+struct RenderArgs {
+  const float* x;        // stage1: source signal y[nx]; else y*f per ear at x + ear*x_pitch
+  long long nx;          // input length
+  long long x_pitch;     // per-ear input stride (stage-2-only mode)
+  const float* f;        // [ears][lf_pad] resonance taps, zero padded (stage1)
+  int lf_pad;            // multiple of 16
+  const int2* taps;      // [ears*dirs][tap_stride]
+  const int* row_nnz;    // [ears*dirs]
+  int tap_stride;        // entries per row (>= max nnz)
+  int uniform_nnz;       // 1 if every row holds exactly tap_stride_nnz taps
+  int tap_stride_nnz;
+  int dirs;              // directions per ear
+  int ears;
+  int dirs_per_group;
+  int groups;            // ceil(dirs / dirs_per_group)
+  int n_tiles;           // ceil(out_len / 2048)
+  long long n_items;     // ears * groups * n_tiles
+  float* out;            // row r at out + r * out_pitch
+  long long out_pitch;   // floats, multiple of 4, >= n_tiles*2048 rounded down to 512 granularity
+  long long out_len;
+};
+
+int render_kwin_for(int K);
+size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int dpg, int tap_stride);
+cudaError_t launch_render(const RenderArgs& a, int kwin, bool stage1, int sm_count, cudaStream_t st);
+
+// Dense FIR, one filter per channel: out[c][t] = sum_j h[c][j] x[c][t-j], t < out_len.
+struct FirArgs {
+  const float* x;
+  long long nx;
+  long long x_pitch;
+  const float* h;        // [channels][h_pitch] zero padded to a multiple of 16
+  int nh_pad;
+  int h_pitch;
+  float* out;
+  long long out_len;
+  long long out_pitch;
+  int channels;
+};
+cudaError_t launch_fir(const FirArgs& a, cudaStream_t st);
+
+// Generic sparse convolution for long reflection filters (K > 497): banded
+// shared-memory gather.  Same tap encoding but col = raw offset.
+struct SparseGenericArgs {
+  const float* x;
+  long long nx;
+  long long x_pitch;     // input stride between row groups (0 = shared input)
+  int rows_per_x;        // consecutive rows sharing one input (>= 1)
+  const int2* taps;      // raw offsets
+  const int* row_nnz;
+  int tap_stride;
+  int rows;
+  float* out;
+  long long out_len;
+  long long out_pitch;
+};
+cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st);
+
+// Source -> per-ear partial mix, reflection filters first (g-first order):
+//   part[grp][e][t] = sum_{s in grp} sum_k v_{e,d(s),k} * y_s[t - o_{e,d(s),k}]
+struct MixArgs {
+  const float* y;        // sources, row s at y + s * y_pitch, length T
+  long long T;
+  long long y_pitch;
+  const int* src_dir;    // [S] direction of each source
+  int S;
+  const int2* taps;      // same tables as RenderArgs (col = KWIN - o)
+  const int* row_nnz;
+  int tap_stride;
+  int uniform_nnz;
+  int dirs;
+  int ears;
+  int src_per_group;
+  int groups;
+  int n_tiles;           // ceil(zlen / 2048)
+  long long n_items;     // groups * n_tiles
+  float* part;           // [groups][ears][part_pitch]
+  long long part_pitch;
+  long long zlen;        // T + K - 1
+};
+cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st);
+
+// z[e][t] = sum_g part[g][e][t]  (fixed order, fp32)
+cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long part_pitch, long long zlen,
+                              float* z, long long z_pitch, cudaStream_t st);
+
+// Streaming block step (g-first, carried history).
+struct StreamArgs {
+  const float* block;    // [S][B] new samples
+  int B;
+  float* yhist;          // [S][H] last H samples of every source (H >= K-1, multiple of 4)
+  int H;
+  const int* src_dir;
+  int S;
+  const int2* taps;      // raw offsets (col = o)
+  const int* row_nnz;
+  int tap_stride;
+  int dirs;
+  int ears;
+  int src_per_cta;
+  float* part;           // [ctas][ears][B]
+  float* zhist;          // [ears][lf_pad] last lf_pad-? samples of z (H2 >= Lf-1)
+  int zh;                // history length of z (multiple of 16, >= Lf-1)
+  const float* f;        // [ears][lf_pad]
+  int lf_pad;
+  float* out;            // [ears][B]
+  int ctas;
+  unsigned int* ticket;  // zero-initialised device counter owned by the stream state
+};
+cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st);
+
+}  // namespace toep

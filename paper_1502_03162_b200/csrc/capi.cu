@@ -209,10 +209,11 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const float* x,
     a.dirs = nrows;
     a.ears = 1;
     const int budget_taps = 2048;  // int2 entries staged per group (16 KB)
-    a.dirs_per_group = std::max(1, std::min(nrows, budget_taps / t->tap_stride));
-    a.groups = (nrows + a.dirs_per_group - 1) / a.dirs_per_group;
+    const int dpg_max = std::max(1, std::min(nrows, budget_taps / t->tap_stride));
+    a.groups = (nrows + dpg_max - 1) / dpg_max;
+    a.dirs_per_group = (nrows + a.groups - 1) / a.groups;  // group sizes are q or q+1
     a.n_tiles = (int)((out_len + kW - 1) / kW);
-    a.n_items = (long long)a.groups * a.n_tiles;
+    a.n_items = (long long)nrows * a.n_tiles;  // work units (direction x tile)
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;
@@ -313,7 +314,7 @@ static int render_dirs_per_group(const toep_renderer* r) {
   const int kwin = r->g->kwin;
   const int per_sm = 512 / (kR + kwin);
   const int budget = 227 * 1024 / per_sm - 1024;
-  int dpg = std::min(r->dirs, std::max(1, 4096 / r->g->tap_stride));
+  int dpg = std::min(r->dirs, std::max(1, 2048 / r->g->tap_stride));
   while (dpg > 1 && (int)render_smem_bytes(kwin, true, r->lf_pad, dpg, r->g->tap_stride) > budget) dpg = (dpg + 1) / 2;
   return dpg;
 }
@@ -390,10 +391,11 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.tap_stride_nnz = g->tap_stride;
     a.dirs = r->dirs;
     a.ears = r->ears;
-    a.dirs_per_group = render_dirs_per_group(r);
-    a.groups = (r->dirs + a.dirs_per_group - 1) / a.dirs_per_group;
+    const int dpg_max = render_dirs_per_group(r);
+    a.groups = (r->dirs + dpg_max - 1) / dpg_max;
+    a.dirs_per_group = (r->dirs + a.groups - 1) / a.groups;  // group sizes are q or q+1
     a.n_tiles = (int)((out_len + kW - 1) / kW);
-    a.n_items = (long long)a.ears * a.groups * a.n_tiles;
+    a.n_items = (long long)a.ears * a.dirs * a.n_tiles;  // work units (direction x tile)
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;

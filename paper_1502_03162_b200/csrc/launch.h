@@ -30,7 +30,7 @@ struct RenderArgs {
   int dirs_per_group;
   int groups;            // ceil(dirs / dirs_per_group)
   int n_tiles;           // ceil(out_len / 2048)
-  long long n_items;     // ears * groups * n_tiles
+  long long n_items;     // work units: ears * dirs * n_tiles
   float* out;            // row r at out + r * out_pitch
   long long out_pitch;   // floats, multiple of 4, >= n_tiles*2048 rounded down to 512 granularity
   long long out_len;

@@ -34,10 +34,14 @@ struct SmemLayout {
   int x_off, f_off, yf_off, stage_off, taps_off, nnz_off, total;
 };
 
+// Tap tables are staged per (ear, group) as direction *pairs*: entry
+// [pair][k] = int4 {colA, vA, colB, vB}, so one LDS.128 feeds two independent
+// TMEM-load/FFMA chains (two directions rendered together per warp).
 __host__ __device__ inline SmemLayout render_smem_layout(int KWIN, bool stage1, int lf_pad, int dpg,
                                                          int tap_stride) {
   SmemLayout L{};
   const int YH = KWIN + kR;
+  const int pairs = (dpg + 1) / 2;
   int off = 0;
   L.x_off = off;
   if (stage1) off += padded_len(kW + YH + lf_pad);
@@ -49,69 +53,109 @@ __host__ __device__ inline SmemLayout render_smem_layout(int KWIN, bool stage1, 
   off += kW + YH;
   off = (off + 31) & ~31;
   L.stage_off = off;
-  off += kWarps * 2 * 32 * kR;
-  L.taps_off = off;  // int2 entries (8 B) -> counted in floats x2
-  off += 2 * dpg * tap_stride;
+  off += kWarps * 2 * 32 * kR;        // one pair-slot (2 x 512 floats) per warp
+  L.taps_off = off;                   // int4 entries (16 B) -> 4 floats each
+  off += 4 * pairs * tap_stride;
   L.nnz_off = off;
-  off += dpg;
+  off += 2 * pairs;
   L.total = off * 4 + 16;
   return L;
 }
+
+// Balanced decomposition: work units are (ear, group, tile, direction) with
+// group sizes nd in {q, q+1}; each persistent CTA takes a contiguous unit range,
+// so CTAs differ by at most one direction-tile of work.
+struct UnitMap {
+  int D, G, q, r, n_tiles;
+  __device__ void decode(long long u, int& e, int& g, int& j, int& dd, int& nd, int& dbeg) const {
+    const long long per_ear = (long long)D * n_tiles;
+    e = (int)(u / per_ear);
+    long long rem = u - (long long)e * per_ear;
+    const long long big = (long long)r * (q + 1) * n_tiles;  // units in the r groups of size q+1
+    long long loc;
+    if (rem < big) {
+      g = (int)(rem / ((long long)(q + 1) * n_tiles));
+      nd = q + 1;
+      loc = rem - (long long)g * (q + 1) * n_tiles;
+      dbeg = g * (q + 1);
+    } else {
+      const long long rr = rem - big;
+      const int gg = (int)(rr / ((long long)q * n_tiles));
+      g = r + gg;
+      nd = q;
+      loc = rr - (long long)gg * q * n_tiles;
+      dbeg = r * (q + 1) + gg * q;
+    }
+    j = (int)(loc / nd);
+    dd = (int)(loc - (long long)j * nd);
+  }
+};
 
 template <int KWIN, bool STAGE1, int NNZT>
 __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_render(RenderArgs a) {
   using C = RenderCfg<KWIN>;
   extern __shared__ __align__(128) float smem[];
   __shared__ unsigned s_tbase;
-  __shared__ long long s_prev_item;
 
   const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.dirs_per_group, a.tap_stride);
   float* s_x = smem + L.x_off;
   float* s_f = smem + L.f_off;
   float* s_yf = smem + L.yf_off;
   float* s_stage = smem + L.stage_off;
-  int2* s_taps = reinterpret_cast<int2*>(smem + L.taps_off);
+  int4* s_taps = reinterpret_cast<int4*>(smem + L.taps_off);
   int* s_nnz = reinterpret_cast<int*>(smem + L.nnz_off);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (warp == 0) tmem_alloc<C::COLS>(&s_tbase);
-  if (tid == 0) s_prev_item = -2;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
 
-  const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
-  const long long it0 = (long long)blockIdx.x * per;
-  const long long it1 = min(a.n_items, it0 + per);
-  int cur_group = -1, cur_ear = -1;
-  int slot = 0;
-  float* my_stage = s_stage + warp * 2 * 32 * kR;
+  UnitMap um;
+  um.D = a.dirs;
+  um.G = a.groups;
+  um.q = a.dirs / a.groups;
+  um.r = a.dirs % a.groups;
+  um.n_tiles = a.n_tiles;
+  const long long n_units = (long long)a.ears * a.dirs * a.n_tiles;
+  const long long u0 = n_units * blockIdx.x / gridDim.x;
+  const long long u1 = n_units * (blockIdx.x + 1) / gridDim.x;
 
-  for (long long item = it0; item < it1; ++item) {
-    const int j = (int)(item % a.n_tiles);
-    const long long eg = item / a.n_tiles;
-    const int g = (int)(eg % a.groups);
-    const int e = (int)(eg / a.groups);
+  int cur_g = -1, cur_e = -1, prev_j = -2;
+  float* st = s_stage + warp * 2 * 32 * kR;
+  const long long out_col = (long long)warp * 32 * kR;  // + T0
+
+  for (long long u = u0; u < u1;) {
+    int e, g, j, dd0, nd, dbeg;
+    um.decode(u, e, g, j, dd0, nd, dbeg);
+    const int dd1 = (int)min((long long)nd, dd0 + (u1 - u));
+    u += dd1 - dd0;
     const long long T0 = (long long)j * kW;
-    const bool reuse_halo = STAGE1 && (item == s_prev_item + 1) && j > 0;
-    const int d_begin = g * a.dirs_per_group;
-    const int nd = min(a.dirs_per_group, a.dirs - d_begin);
+    const bool same_group = (g == cur_g && e == cur_e);
+    const bool reuse_halo = STAGE1 && same_group && (j == prev_j + 1);
 
     __syncthreads();  // previous item fully consumed (TMEM windows, s_yf, s_taps)
 
-    // ---- tap table for (e, g) --------------------------------------------
-    if (g != cur_group || e != cur_ear) {
-      const long long row0 = (long long)e * a.dirs + d_begin;
-      const int n = nd * a.tap_stride;
+    // ---- tap table for (e, g), pair-interleaved ----------------------------
+    if (!same_group) {
+      const long long row0 = (long long)e * a.dirs + dbeg;
+      const int pairs = (nd + 1) / 2;
+      const int n = pairs * a.tap_stride;
       const int2* src = a.taps + row0 * a.tap_stride;
-      for (int i = tid; i < n; i += kThreads) s_taps[i] = src[i];
-      for (int i = tid; i < nd; i += kThreads) s_nnz[i] = a.row_nnz[row0 + i];
-      if (STAGE1 && e != cur_ear)
+      for (int i = tid; i < n; i += kThreads) {
+        const int p = i / a.tap_stride, k = i - p * a.tap_stride;
+        const int2 A = src[(long long)(2 * p) * a.tap_stride + k];
+        const int2 B = (2 * p + 1 < nd) ? src[(long long)(2 * p + 1) * a.tap_stride + k] : make_int2(KWIN, 0);
+        s_taps[i] = make_int4(A.x, A.y, B.x, B.y);
+      }
+      for (int i = tid; i < 2 * pairs; i += kThreads) s_nnz[i] = (i < nd) ? a.row_nnz[row0 + i] : 0;
+      if (STAGE1 && e != cur_e)
         for (int i = tid; i < a.lf_pad; i += kThreads) s_f[i] = a.f[(long long)e * a.lf_pad + i];
-      cur_group = g;
-      cur_ear = e;
+      cur_g = g;
+      cur_e = e;
     }
+    prev_j = j;
 
     // ---- y*f tile [T0 - YH, T0 + kW) -------------------------------------
     if constexpr (STAGE1) {
@@ -155,7 +199,6 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_render(RenderAr
         s_yf[i] = (t >= 0 && t < a.nx) ? __ldg(xe + t) : 0.f;
       }
     }
-    if (tid == 0) s_prev_item = item;
     __syncthreads();
 
     // ---- lane windows -> TMEM ------------------------------------------------
@@ -177,67 +220,88 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_render(RenderAr
       tmem_wait_st();
     }
 
-    // ---- sparse reflection stage ------------------------------------------
-    const long long out_col = T0 + (long long)warp * 32 * kR;
-    const int nd_w = (out_col < a.out_len) ? nd : 0;  // warps wholly past the row end store nothing
-    for (int dd = 0; dd < nd_w; ++dd) {
-      const int2* tp = s_taps + dd * a.tap_stride;
-      float acc[16];
+    // ---- sparse reflection stage, two directions per pass ------------------
+    const long long col = T0 + out_col;
+    if (col >= a.out_len) continue;  // warp wholly past the row end: nothing to store
+    for (int p = dd0 >> 1; 2 * p < dd1; ++p) {
+      const int4* tp = s_taps + p * a.tap_stride;
+      float accA[16], accB[16];
       if constexpr (NNZT > 0) {
-        float A[16], B[16];
-        int2 cur = tp[0];
-        tmem_ld16(A, tlane + cur.x);
 #pragma unroll
         for (int k = 0; k < NNZT; ++k) {
-          const int2 nxt = tp[k + 1 < NNZT ? k + 1 : k];
+          const int4 t = tp[k];
+          float XA[16], XB[16];
+          tmem_ld16(XA, tlane + t.x);
+          tmem_ld16(XB, tlane + t.z);
           tmem_wait_ld();
-          float(&X)[16] = (k & 1) ? B : A;
-          float(&Y)[16] = (k & 1) ? A : B;
-          if (k + 1 < NNZT) tmem_ld16(Y, tlane + nxt.x);
-          const float v = __int_as_float(cur.y);
+          const float va = __int_as_float(t.y), vb = __int_as_float(t.w);
           if (k == 0) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) acc[r] = v * X[r];
+            for (int r = 0; r < 16; ++r) {
+              accA[r] = va * XA[r];
+              accB[r] = vb * XB[r];
+            }
           } else {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) acc[r] = fmaf(v, X[r], acc[r]);
+            for (int r = 0; r < 16; ++r) {
+              accA[r] = fmaf(va, XA[r], accA[r]);
+              accB[r] = fmaf(vb, XB[r], accB[r]);
+            }
           }
-          cur = nxt;
         }
       } else {
-        const int nnz = s_nnz[dd];
+        const int nk = max(s_nnz[2 * p], s_nnz[2 * p + 1]);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) acc[r] = 0.f;
-        float X[16];
-        for (int k = 0; k < nnz; ++k) {
-          const int2 cur = tp[k];
-          tmem_ld16(X, tlane + cur.x);
+        for (int r = 0; r < 16; ++r) {
+          accA[r] = 0.f;
+          accB[r] = 0.f;
+        }
+        for (int k = 0; k < nk; ++k) {
+          const int4 t = tp[k];
+          float XA[16], XB[16];
+          tmem_ld16(XA, tlane + t.x);
+          tmem_ld16(XB, tlane + t.z);
           tmem_wait_ld();
-          const float v = __int_as_float(cur.y);
+          const float va = __int_as_float(t.y), vb = __int_as_float(t.w);
 #pragma unroll
-          for (int r = 0; r < 16; ++r) acc[r] = fmaf(v, X[r], acc[r]);
+          for (int r = 0; r < 16; ++r) {
+            accA[r] = fmaf(va, XA[r], accA[r]);
+            accB[r] = fmaf(vb, XB[r], accB[r]);
+          }
         }
       }
-      // ---- epilogue: registers -> smem slot -> one bulk store per warp --
-      float* st = my_stage + slot * 32 * kR;
-      if (lane == 0) bulk_wait_read<1>();
+      // ---- epilogue: both rows -> smem pair-slot -> bulk stores ---------
+      const int dA = 2 * p, dB = 2 * p + 1;
+      const bool actA = dA >= dd0 && dA < dd1;
+      const bool actB = dB >= dd0 && dB < dd1;
+      if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < 16; r += 4)
-        *reinterpret_cast<float4*>(&st[lane * 16 + r]) = make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]);
-      fence_proxy_async_smem();
-      __syncwarp();
-      {
-        const long long row = (long long)e * a.dirs + d_begin + dd;
-        float* dst = a.out + row * a.out_pitch + out_col;
-        if (out_col + 32 * kR <= a.out_len) {
-          if (lane == 0) bulk_store(dst, st, 32 * kR * 4);
-        } else {  // ragged row end: plain stores, nothing past out_len
-          for (int i = lane; i < 32 * kR; i += 32)
-            if (out_col + i < a.out_len) dst[i] = st[i];
-        }
+      for (int r = 0; r < 16; r += 4) {
+        *reinterpret_cast<float4*>(&st[lane * 16 + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
+        *reinterpret_cast<float4*>(&st[512 + lane * 16 + r]) =
+            make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
       }
-      slot ^= 1;
+      const bool full = col + 32 * kR <= a.out_len;
+      if (full) fence_proxy_async_smem();
+      __syncwarp();
+      const long long rowA = (long long)e * a.dirs + dbeg + dA;
+      float* dstA = a.out + rowA * a.out_pitch + col;
+      float* dstB = dstA + a.out_pitch;
+      if (full) {
+        if (lane == 0) {
+          if (actA) bulk_store(dstA, st, 32 * kR * 4);
+          if (actB) bulk_store(dstB, st + 512, 32 * kR * 4);
+        }
+      } else {  // ragged row end: plain stores, nothing past out_len
+        for (int i = lane; i < 32 * kR; i += 32) {
+          if (col + i < a.out_len) {
+            if (actA) dstA[i] = st[i];
+            if (actB) dstB[i] = st[512 + i];
+          }
+        }
+        __syncwarp();
+      }
     }
   }
   if (lane == 0) bulk_wait_all();

@@ -23,7 +23,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2",
     "-cudart", "static",
     "-diag-suppress", "177",
-]
+] + os.environ.get("TOEP_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

@@ -20,6 +20,10 @@
 #include "common.cuh"
 #include "launch.h"
 
+#ifndef TOEP_RENDER_MINB
+#define TOEP_RENDER_MINB 4
+#endif
+
 namespace toep {
 
 template <int KWIN>
@@ -92,7 +96,7 @@ struct UnitMap {
 };
 
 template <int KWIN, bool STAGE1, int NNZT>
-__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_render(RenderArgs a) {
+__global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDER_MINB : (512 / (kR + KWIN))) k_render(RenderArgs a) {
   using C = RenderCfg<KWIN>;
   extern __shared__ __align__(128) float smem[];
   __shared__ unsigned s_tbase;
@@ -227,13 +231,24 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_render(RenderAr
       const int4* tp = s_taps + p * a.tap_stride;
       float accA[16], accB[16];
       if constexpr (NNZT > 0) {
+        // software pipeline: the TMEM loads of tap k+1 are in flight while
+        // tap k's 32 FFMA issue (tcgen05.wait::ld only ever waits for tap k)
+        float XA0[16], XB0[16], XA1[16], XB1[16];
+        int4 t = tp[0];
+        tmem_ld16(XA0, tlane + t.x);
+        tmem_ld16(XB0, tlane + t.z);
 #pragma unroll
         for (int k = 0; k < NNZT; ++k) {
-          const int4 t = tp[k];
-          float XA[16], XB[16];
-          tmem_ld16(XA, tlane + t.x);
-          tmem_ld16(XB, tlane + t.z);
+          const int4 tn = tp[k + 1 < NNZT ? k + 1 : k];
+          float(&XA)[16] = (k & 1) ? XA1 : XA0;
+          float(&XB)[16] = (k & 1) ? XB1 : XB0;
+          float(&YA)[16] = (k & 1) ? XA0 : XA1;
+          float(&YB)[16] = (k & 1) ? XB0 : XB1;
           tmem_wait_ld();
+          if (k + 1 < NNZT) {
+            tmem_ld16(YA, tlane + tn.x);
+            tmem_ld16(YB, tlane + tn.z);
+          }
           const float va = __int_as_float(t.y), vb = __int_as_float(t.w);
           if (k == 0) {
 #pragma unroll
@@ -248,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_render(RenderAr
               accB[r] = fmaf(vb, XB[r], accB[r]);
             }
           }
+          t = tn;
         }
       } else {
         const int nk = max(s_nnz[2 * p], s_nnz[2 * p + 1]);

@@ -217,7 +217,10 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const float* x,
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;
-    cudaError_t e = launch_render(a, t->kwin, false, sm_count_cached(), st);
+    RenderMaps maps;
+    cudaError_t e = make_render_maps(out, nrows, out_len, out_pitch, &maps);
+    if (e != cudaSuccess) return cuda_fail(e, "tensor map (output rows)");
+    e = launch_render(a, maps, t->kwin, false, sm_count_cached(), st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_render(stage 2)");
     return TOEP_OK;
   }
@@ -399,7 +402,10 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;
-    cudaError_t e = launch_render(a, g->kwin, true, sm_count_cached(), st);
+    RenderMaps maps;
+    cudaError_t e = make_render_maps(out, rows, out_len, out_pitch, &maps);
+    if (e != cudaSuccess) return cuda_fail(e, "tensor map (output rows)");
+    e = launch_render(a, maps, g->kwin, true, sm_count_cached(), st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_render");
     return TOEP_OK;
   }

@@ -1,6 +1,7 @@
 // Internal launcher interface between the C ABI (capi.cu) and the kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace toep {
@@ -36,9 +37,18 @@ struct RenderArgs {
   long long out_len;
 };
 
+// TMA tensor maps over the output rows ([rows][out_len], row stride out_pitch):
+// box {256, 2} for direction pairs and {256, 1} for a trailing odd direction.
+struct RenderMaps {
+  alignas(64) CUtensorMap rows2;
+  alignas(64) CUtensorMap rows1;
+};
+
 int render_kwin_for(int K);
 size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int dpg, int tap_stride);
-cudaError_t launch_render(const RenderArgs& a, int kwin, bool stage1, int sm_count, cudaStream_t st);
+cudaError_t make_render_maps(float* out, long long rows, long long out_len, long long out_pitch, RenderMaps* m);
+cudaError_t launch_render(const RenderArgs& a, const RenderMaps& m, int kwin, bool stage1, int sm_count,
+                          cudaStream_t st);
 
 // Dense FIR, one filter per channel: out[c][t] = sum_j h[c][j] x[c][t-j], t < out_len.
 struct FirArgs {

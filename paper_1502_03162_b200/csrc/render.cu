@@ -35,42 +35,48 @@ struct RenderCfg {
 };
 
 struct SmemLayout {
-  int x_off, f_off, yf_off, stage_off, taps_off, nnz_off, total;
+  int region_off, x_off, yf_off, halo_off, f_off, taps_off, nnz_off, total;
 };
 
+constexpr int kStageFloatsPerWarp = 4 * 32 * kR;  // 4 directions x 512 outputs
+
+// Shared memory plan.  The stage-1 input tile (s_x) and the y*f tile (s_yf)
+// are only live between an item's start and its TMEM window write, the bulk
+// store staging only during its direction loop, so they share one region.
 // Tap tables are staged per (ear, group) as direction *pairs*: entry
-// [pair][k] = int4 {colA, vA, colB, vB}, so one LDS.128 feeds two independent
-// TMEM-load/FFMA chains (two directions rendered together per warp).
+// [pair][k] = int4 {colA, vA, colB, vB}, so one LDS.128 feeds two
+// independent TMEM-load/FFMA chains.
 __host__ __device__ inline SmemLayout render_smem_layout(int KWIN, bool stage1, int lf_pad, int dpg,
                                                          int tap_stride) {
   SmemLayout L{};
   const int YH = KWIN + kR;
   const int pairs = (dpg + 1) / 2;
-  int off = 0;
-  L.x_off = off;
-  if (stage1) off += padded_len(kW + YH + lf_pad);
-  off = (off + 31) & ~31;
+  L.region_off = 0;
+  L.x_off = 0;
+  int tile = stage1 ? ((padded_len(kW + YH + lf_pad) + 31) & ~31) : 0;
+  L.yf_off = tile;
+  tile += kW + YH;
+  int region = tile > kWarps * kStageFloatsPerWarp ? tile : kWarps * kStageFloatsPerWarp;
+  int off = (region + 31) & ~31;
+  L.halo_off = off;
+  off += (YH + 31) & ~31;
   L.f_off = off;
-  if (stage1) off += lf_pad;
-  off = (off + 31) & ~31;
-  L.yf_off = off;
-  off += kW + YH;
-  off = (off + 31) & ~31;
-  L.stage_off = off;
-  off += kWarps * 2 * 32 * kR;        // one pair-slot (2 x 512 floats) per warp
-  L.taps_off = off;                   // int4 entries (16 B) -> 4 floats each
+  off += (lf_pad + 31) & ~31;
+  L.taps_off = off;  // int4 entries -> 4 floats each
   off += 4 * pairs * tap_stride;
   L.nnz_off = off;
   off += 2 * pairs;
-  L.total = off * 4 + 16;
+  L.total = off * 4 + 1024;  // + alignment slack for the 1 KB-aligned base
   return L;
 }
 
 // Balanced decomposition: work units are (ear, group, tile, direction) with
-// group sizes nd in {q, q+1}; each persistent CTA takes a contiguous unit range,
-// so CTAs differ by at most one direction-tile of work.
+// group sizes nd in {q, q+1}; each persistent CTA takes a contiguous unit
+// range snapped to even directions (pairs are never split between CTAs), so
+// CTAs differ by at most one direction pair of one tile.
 struct UnitMap {
   int D, G, q, r, n_tiles;
+  long long n_units;
   __device__ void decode(long long u, int& e, int& g, int& j, int& dd, int& nd, int& dbeg) const {
     const long long per_ear = (long long)D * n_tiles;
     e = (int)(u / per_ear);
@@ -93,19 +99,33 @@ struct UnitMap {
     j = (int)(loc / nd);
     dd = (int)(loc - (long long)j * nd);
   }
+  __device__ long long snap(long long u) const {
+    if (u >= n_units) return n_units;
+    int e, g, j, dd, nd, dbeg;
+    decode(u, e, g, j, dd, nd, dbeg);
+    return u - (dd & 1);
+  }
 };
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const float* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tm),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
 template <int KWIN, bool STAGE1, int NNZT>
-__global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDER_MINB : (512 / (kR + KWIN))) k_render(RenderArgs a) {
+__global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDER_MINB : (512 / (kR + KWIN)))
+    k_render(RenderArgs a, const __grid_constant__ CUtensorMap tm2, const __grid_constant__ CUtensorMap tm1) {
   using C = RenderCfg<KWIN>;
-  extern __shared__ __align__(128) float smem[];
+  extern __shared__ float smem_raw[];
   __shared__ unsigned s_tbase;
+  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.dirs_per_group, a.tap_stride);
   float* s_x = smem + L.x_off;
-  float* s_f = smem + L.f_off;
   float* s_yf = smem + L.yf_off;
-  float* s_stage = smem + L.stage_off;
+  float* s_halo = smem + L.halo_off;
+  float* s_f = smem + L.f_off;
   int4* s_taps = reinterpret_cast<int4*>(smem + L.taps_off);
   int* s_nnz = reinterpret_cast<int*>(smem + L.nnz_off);
 
@@ -122,13 +142,13 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
   um.q = a.dirs / a.groups;
   um.r = a.dirs % a.groups;
   um.n_tiles = a.n_tiles;
-  const long long n_units = (long long)a.ears * a.dirs * a.n_tiles;
-  const long long u0 = n_units * blockIdx.x / gridDim.x;
-  const long long u1 = n_units * (blockIdx.x + 1) / gridDim.x;
+  um.n_units = (long long)a.ears * a.dirs * a.n_tiles;
+  const long long u0 = um.snap(um.n_units * blockIdx.x / gridDim.x);
+  const long long u1 = um.snap(um.n_units * (blockIdx.x + 1) / gridDim.x);
 
   int cur_g = -1, cur_e = -1, prev_j = -2;
-  float* st = s_stage + warp * 2 * 32 * kR;
-  const long long out_col = (long long)warp * 32 * kR;  // + T0
+  float* st = smem + L.region_off + warp * kStageFloatsPerWarp;
+  const int half = lane >> 4, inner = (lane & 15) * 16;
 
   for (long long u = u0; u < u1;) {
     int e, g, j, dd0, nd, dbeg;
@@ -139,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
     const bool same_group = (g == cur_g && e == cur_e);
     const bool reuse_halo = STAGE1 && same_group && (j == prev_j + 1);
 
-    __syncthreads();  // previous item fully consumed (TMEM windows, s_yf, s_taps)
+    if (lane == 0) bulk_wait_read<0>();  // staging region is about to be reused
+    __syncthreads();  // previous item fully consumed (TMEM windows, smem region, s_taps)
 
     // ---- tap table for (e, g), pair-interleaved ----------------------------
     if (!same_group) {
@@ -169,10 +190,8 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
         const long long t = xs + i;
         s_x[padi(i)] = (t >= 0 && t < a.nx) ? __ldg(a.x + t) : 0.f;
       }
-      if (reuse_halo) {
-        // last YH values of the previous tile become this tile's halo
-        for (int i = tid; i < C::YH; i += kThreads) s_yf[i] = s_yf[kW + i];
-      }
+      if (reuse_halo)  // last YH values of the previous tile are this tile's halo
+        for (int i = tid; i < C::YH; i += kThreads) s_yf[i] = s_halo[i];
       __syncthreads();
       if (!reuse_halo) {
         for (int c = tid; c < C::YH / 16; c += kThreads) {
@@ -205,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
     }
     __syncthreads();
 
-    // ---- lane windows -> TMEM ------------------------------------------------
+    // ---- lane windows -> TMEM; keep the next tile's halo -----------------
     {
       const int wbase = (C::YH - KWIN) + 16 * tid;  // = 16 + 16*tid
 #pragma unroll
@@ -221,13 +240,17 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
         }
         tmem_st16(tlane + c, v);
       }
+      if (STAGE1)
+        for (int i = tid; i < C::YH; i += kThreads) s_halo[i] = s_yf[kW + i];
       tmem_wait_st();
     }
+    __syncthreads();  // s_yf fully read: the region becomes bulk-store staging
 
     // ---- sparse reflection stage, two directions per pass ------------------
-    const long long col = T0 + out_col;
+    const long long col = T0 + (long long)warp * 32 * kR;
     if (col >= a.out_len) continue;  // warp wholly past the row end: nothing to store
-    for (int p = dd0 >> 1; 2 * p < dd1; ++p) {
+    const int p0 = dd0 >> 1, p1 = (dd1 + 1) >> 1;
+    for (int p = p0; p < p1; ++p) {
       const int4* tp = s_taps + p * a.tap_stride;
       float accA[16], accB[16];
       if constexpr (NNZT > 0) {
@@ -235,19 +258,21 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
         // tap k's 32 FFMA issue (tcgen05.wait::ld only ever waits for tap k)
         float XA0[16], XB0[16], XA1[16], XB1[16];
         int4 t = tp[0];
+        int4 tn = tp[NNZT > 1 ? 1 : 0];  // taps are read two ahead of their TMEM loads
         tmem_ld16(XA0, tlane + t.x);
         tmem_ld16(XB0, tlane + t.z);
 #pragma unroll
         for (int k = 0; k < NNZT; ++k) {
-          const int4 tn = tp[k + 1 < NNZT ? k + 1 : k];
+          const int4 tnn = tp[k + 2 < NNZT ? k + 2 : NNZT - 1];
           float(&XA)[16] = (k & 1) ? XA1 : XA0;
           float(&XB)[16] = (k & 1) ? XB1 : XB0;
           float(&YA)[16] = (k & 1) ? XA0 : XA1;
           float(&YB)[16] = (k & 1) ? XB0 : XB1;
+          const unsigned na = tlane + tn.x, nb = tlane + tn.z;
           tmem_wait_ld();
           if (k + 1 < NNZT) {
-            tmem_ld16(YA, tlane + tn.x);
-            tmem_ld16(YB, tlane + tn.z);
+            tmem_ld16(YA, na);
+            tmem_ld16(YB, nb);
           }
           const float va = __int_as_float(t.y), vb = __int_as_float(t.w);
           if (k == 0) {
@@ -264,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
             }
           }
           t = tn;
+          tn = tnn;
         }
       } else {
         const int nk = max(s_nnz[2 * p], s_nnz[2 * p + 1]);
@@ -286,37 +312,36 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
           }
         }
       }
-      // ---- epilogue: both rows -> smem pair-slot -> bulk stores ---------
-      const int dA = 2 * p, dB = 2 * p + 1;
-      const bool actA = dA >= dd0 && dA < dd1;
-      const bool actB = dB >= dd0 && dB < dd1;
-      if (lane == 0) bulk_wait_read<0>();
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 16; r += 4) {
-        *reinterpret_cast<float4*>(&st[lane * 16 + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
-        *reinterpret_cast<float4*>(&st[512 + lane * 16 + r]) =
-            make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
-      }
-      const bool full = col + 32 * kR <= a.out_len;
-      if (full) fence_proxy_async_smem();
-      __syncwarp();
-      const long long rowA = (long long)e * a.dirs + dbeg + dA;
-      float* dstA = a.out + rowA * a.out_pitch + col;
-      float* dstB = dstA + a.out_pitch;
-      if (full) {
-        if (lane == 0) {
-          if (actA) bulk_store(dstA, st, 32 * kR * 4);
-          if (actB) bulk_store(dstB, st + 512, 32 * kR * 4);
-        }
-      } else {  // ragged row end: plain stores, nothing past out_len
-        for (int i = lane; i < 32 * kR; i += 32) {
-          if (col + i < a.out_len) {
-            if (actA) dstA[i] = st[i];
-            if (actB) dstB[i] = st[512 + i];
-          }
-        }
+      // ---- epilogue: stage 2 pairs (4 rows), then one proxy fence and
+      //      TMA tensor stores of [2 rows x 256] boxes (clipped at out_len)
+      const int pp = (p - p0) & 1;
+      if (pp == 0) {
+        if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
+      }
+      {
+        float* box = st + (pp * 2 + half) * 512;  // [row][256]
+#pragma unroll
+        for (int r = 0; r < 16; r += 4) {
+          *reinterpret_cast<float4*>(&box[inner + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
+          *reinterpret_cast<float4*>(&box[256 + inner + r]) =
+              make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
+        }
+      }
+      if (pp == 1 || p + 1 == p1) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          for (int q = 0; q <= pp; ++q) {
+            const int pq = p - pp + q;
+            const int rowA = e * a.dirs + dbeg + 2 * pq;
+            const CUtensorMap* tm = (2 * pq + 1 < nd) ? &tm2 : &tm1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (col + 256 * h < a.out_len) tma_store_2d(tm, st + (q * 2 + h) * 512, (int)(col + 256 * h), rowA);
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     }
   }
@@ -328,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
 
 // ---------------------------------------------------------------- launch ----
 template <int KWIN, bool STAGE1, int NNZT>
-static cudaError_t launch_render_t(const RenderArgs& a, int sm_count, cudaStream_t st) {
+static cudaError_t launch_render_t(const RenderArgs& a, const RenderMaps& m, int sm_count, cudaStream_t st) {
   using C = RenderCfg<KWIN>;
   const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.dirs_per_group, a.tap_stride);
   auto kern = k_render<KWIN, STAGE1, NNZT>;
@@ -338,26 +363,61 @@ static cudaError_t launch_render_t(const RenderArgs& a, int sm_count, cudaStream
   // and registers are sized so the hardware never exceeds that.
   const int per_sm = 512 / C::COLS;
   long long grid = (long long)sm_count * per_sm;
-  if (grid > a.n_items) grid = a.n_items;
+  const long long pairs_total = (a.n_items + 1) / 2;
+  if (grid > pairs_total) grid = pairs_total;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kThreads, L.total, st>>>(a);
+  kern<<<(unsigned)grid, kThreads, L.total, st>>>(a, m.rows2, m.rows1);
   return cudaGetLastError();
 }
 
 template <int KWIN, bool STAGE1>
-static cudaError_t dispatch_nnz(const RenderArgs& a, int sm, cudaStream_t st) {
+static cudaError_t dispatch_nnz(const RenderArgs& a, const RenderMaps& m, int sm, cudaStream_t st) {
   if (a.uniform_nnz) {
     switch (a.tap_stride_nnz) {
-      case 4: return launch_render_t<KWIN, STAGE1, 4>(a, sm, st);
-      case 8: return launch_render_t<KWIN, STAGE1, 8>(a, sm, st);
-      case 12: return launch_render_t<KWIN, STAGE1, 12>(a, sm, st);
-      case 16: return launch_render_t<KWIN, STAGE1, 16>(a, sm, st);
-      case 24: return launch_render_t<KWIN, STAGE1, 24>(a, sm, st);
-      case 32: return launch_render_t<KWIN, STAGE1, 32>(a, sm, st);
+      case 4: return launch_render_t<KWIN, STAGE1, 4>(a, m, sm, st);
+      case 8: return launch_render_t<KWIN, STAGE1, 8>(a, m, sm, st);
+      case 12: return launch_render_t<KWIN, STAGE1, 12>(a, m, sm, st);
+      case 16: return launch_render_t<KWIN, STAGE1, 16>(a, m, sm, st);
+      case 24: return launch_render_t<KWIN, STAGE1, 24>(a, m, sm, st);
+      case 32: return launch_render_t<KWIN, STAGE1, 32>(a, m, sm, st);
       default: break;
     }
   }
-  return launch_render_t<KWIN, STAGE1, 0>(a, sm, st);
+  return launch_render_t<KWIN, STAGE1, 0>(a, m, sm, st);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+cudaError_t make_render_maps(float* out, long long rows, long long out_len, long long out_pitch, RenderMaps* m) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) || (rows > 1 && (out_pitch * 4) % 16)) return cudaErrorInvalidValue;
+  const cuuint64_t dims[2] = {(cuuint64_t)out_len, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(rows > 1 ? out_pitch : ((out_len + 3) / 4 * 4)) * 4};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int b = 0; b < 2; ++b) {
+    const cuuint32_t box[2] = {256, (cuuint32_t)(b == 0 && rows > 1 ? 2 : 1)};
+    CUresult r = enc(b == 0 ? &m->rows2 : &m->rows1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
 }
 
 int render_kwin_for(int K) {
@@ -371,18 +431,19 @@ size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int dpg, int tap_str
   return (size_t)render_smem_layout(kwin, stage1, lf_pad, dpg, tap_stride).total;
 }
 
-cudaError_t launch_render(const RenderArgs& a, int kwin, bool stage1, int sm_count, cudaStream_t st) {
+cudaError_t launch_render(const RenderArgs& a, const RenderMaps& m, int kwin, bool stage1, int sm_count,
+                          cudaStream_t st) {
   if (stage1) {
     switch (kwin) {
-      case 112: return dispatch_nnz<112, true>(a, sm_count, st);
-      case 240: return dispatch_nnz<240, true>(a, sm_count, st);
-      case 496: return dispatch_nnz<496, true>(a, sm_count, st);
+      case 112: return dispatch_nnz<112, true>(a, m, sm_count, st);
+      case 240: return dispatch_nnz<240, true>(a, m, sm_count, st);
+      case 496: return dispatch_nnz<496, true>(a, m, sm_count, st);
     }
   } else {
     switch (kwin) {
-      case 112: return dispatch_nnz<112, false>(a, sm_count, st);
-      case 240: return dispatch_nnz<240, false>(a, sm_count, st);
-      case 496: return dispatch_nnz<496, false>(a, sm_count, st);
+      case 112: return dispatch_nnz<112, false>(a, m, sm_count, st);
+      case 240: return dispatch_nnz<240, false>(a, m, sm_count, st);
+      case 496: return dispatch_nnz<496, false>(a, m, sm_count, st);
     }
   }
   return cudaErrorInvalidValue;

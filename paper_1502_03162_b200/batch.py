@@ -63,6 +63,7 @@ class _ModelSet:
         if not np.all(np.isfinite(f)):
             raise DataError("taps contain non-finite values")
         self.rows = model_rows(self.models)
+        _lib.require_cuda()  # no host fallback: fail before building device state
         self.row_nnz = np.array([r[0].size for r in self.rows], dtype=np.int64)
         self.taps = _lib.Taps(self.rows, self.K)
         self.native = _lib.NativeRenderer(f, self.taps, self.dirs)

@@ -99,7 +99,7 @@ static int taps_build(int32_t rows, int32_t length, const int64_t* row_ptr, cons
   t->max_nnz = max_nnz;
   t->total = row_ptr[rows];
   t->kwin = render_kwin_for(length);
-  t->tap_stride = std::max(1, max_nnz);
+  t->tap_stride = std::max(2, (max_nnz + 1) & ~1);  // even: tap rows are whole 16-byte units (bulk copies)
   t->uniform = (uni && uniform_supported(max_nnz)) ? 1 : 0;
   t->stream_owned = stream_owned;
   t->owner = st;
@@ -205,7 +205,7 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const float* x,
     a.row_nnz = t->d_nnz + row0;
     a.tap_stride = t->tap_stride;
     a.uniform_nnz = t->uniform;
-    a.tap_stride_nnz = t->tap_stride;
+    a.tap_stride_nnz = t->max_nnz;
     a.dirs = nrows;
     a.ears = 1;
     const int budget_taps = 2048;  // int2 entries staged per group (16 KB)
@@ -391,7 +391,7 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.row_nnz = g->d_nnz;
     a.tap_stride = g->tap_stride;
     a.uniform_nnz = g->uniform;
-    a.tap_stride_nnz = g->tap_stride;
+    a.tap_stride_nnz = g->max_nnz;
     a.dirs = r->dirs;
     a.ears = r->ears;
     const int dpg_max = render_dirs_per_group(r);
@@ -454,6 +454,9 @@ struct toep_mixer {
   int S = 0;
   long long T = 0, zlen = 0;
   int* d_dir = nullptr;
+  std::vector<int> h_dir;
+  int4* d_steps = nullptr;      // direction-sorted step table of the last [s0, s0+count) range
+  int order_s0 = -1, order_count = -1;
   float* d_part = nullptr;
   size_t part_bytes = 0;
 };
@@ -480,7 +483,9 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
   m->S = n_src;
   m->T = T;
   m->zlen = T + r->g->length - 1;
+  m->h_dir.assign(src_dir_host, src_dir_host + n_src);
   cudaError_t e = cudaMalloc(&m->d_dir, n_src * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_steps, n_src * sizeof(int4));
   if (e == cudaSuccess) e = cudaMemcpy(m->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     toep_mixer_destroy(m);
@@ -493,6 +498,7 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
 int toep_mixer_destroy(toep_mixer* m) {
   if (!m) return TOEP_OK;
   if (m->d_dir) cudaFree(m->d_dir);
+  if (m->d_steps) cudaFree(m->d_steps);
   if (m->d_part) cudaFree(m->d_part);
   delete m;
   return TOEP_OK;
@@ -507,6 +513,8 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   if (count < 1 || s0 < 0 || (long long)s0 + count > m->S) return fail(TOEP_ERR_INVALID, "source range out of bounds");
   if (!y || !z) return fail(TOEP_ERR_INVALID, "null buffer");
   if (count > 1 && y_pitch < m->T) return fail(TOEP_ERR_INVALID, "source pitch too small");
+  if ((reinterpret_cast<uintptr_t>(y) & 15) || (count > 1 && y_pitch % 4))
+    return fail(TOEP_ERR_INVALID, "sources must be 16-byte aligned with a pitch multiple of 4");
   if (m->r->ears > 1 && z_pitch < m->zlen) return fail(TOEP_ERR_INVALID, "z pitch too small");
   cudaStream_t st = S(stream);
   const toep_taps* g = m->r->g;
@@ -524,8 +532,28 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     TOEP_CUDA(cudaMalloc(&m->d_part, need));
     m->part_bytes = need;
   }
+  if (s0 != m->order_s0 || count != m->order_count) {
+    // stable sort of the range by direction; per sorted position {src, dir, first, last}
+    // within its group: sources sharing a direction are summed before their taps
+    std::vector<int> ord(count);
+    for (int i = 0; i < count; ++i) ord[i] = i;
+    const int* dir = m->h_dir.data() + s0;
+    std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
+    std::vector<int4> steps(count);
+    for (int p = 0; p < count; ++p) {
+      const int d = dir[ord[p]];
+      const bool first = (p % kSrcPerGroup == 0) || dir[ord[p - 1]] != d;
+      const bool last = ((p + 1) % kSrcPerGroup == 0) || p + 1 == count || dir[ord[p + 1]] != d;
+      steps[p] = make_int4(ord[p], d, first ? 1 : 0, last ? 1 : 0);
+    }
+    TOEP_CUDA(cudaMemcpyAsync(m->d_steps, steps.data(), count * sizeof(int4), cudaMemcpyHostToDevice, st));
+    TOEP_CUDA(cudaStreamSynchronize(st));
+    m->order_s0 = s0;
+    m->order_count = count;
+  }
   MixArgs a{};
   a.y = y;
+  a.steps = m->d_steps;
   a.T = m->T;
   a.y_pitch = y_pitch;
   a.src_dir = m->d_dir + s0;
@@ -534,6 +562,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   a.row_nnz = g->d_nnz;
   a.tap_stride = g->tap_stride;
   a.uniform_nnz = g->uniform;
+  a.tap_stride_nnz = g->max_nnz;
   a.dirs = m->r->dirs;
   a.ears = m->r->ears;
   a.src_per_group = kSrcPerGroup;

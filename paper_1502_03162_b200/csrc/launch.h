@@ -89,11 +89,13 @@ struct MixArgs {
   long long T;
   long long y_pitch;
   const int* src_dir;    // [S] direction of each source
+  const int4* steps;     // [S] direction-sorted {src, dir, first-of-dir, last-of-dir} per group position
   int S;
-  const int2* taps;      // same tables as RenderArgs (col = KWIN - o)
+  const int2* taps;      // same tables as RenderArgs (col = KWIN - o); tap_stride even
   const int* row_nnz;
   int tap_stride;
   int uniform_nnz;
+  int tap_stride_nnz;    // taps per row when uniform_nnz
   int dirs;
   int ears;
   int src_per_group;

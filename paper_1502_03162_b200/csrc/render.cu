@@ -373,7 +373,7 @@ static cudaError_t launch_render_t(const RenderArgs& a, const RenderMaps& m, int
 template <int KWIN, bool STAGE1>
 static cudaError_t dispatch_nnz(const RenderArgs& a, const RenderMaps& m, int sm, cudaStream_t st) {
   if (a.uniform_nnz) {
-    switch (a.tap_stride_nnz) {
+    switch (a.tap_stride_nnz) {  // == max nnz (all rows equal)
       case 4: return launch_render_t<KWIN, STAGE1, 4>(a, m, sm, st);
       case 8: return launch_render_t<KWIN, STAGE1, 8>(a, m, sm, st);
       case 12: return launch_render_t<KWIN, STAGE1, 12>(a, m, sm, st);

@@ -9,6 +9,8 @@
 //                      (tests/test_acceptance.py:283-300):
 //                      sum_s (y_s*f_e)*g_s,e = f_e * sum_s (y_s*g_s,e)
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -117,41 +119,37 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st) {
 
 // ----------------------------------------------------------- g-first mix ----
 // Work item = (source group, time tile).  Sources are visited in direction-
-// sorted order (a.order), and the time tiles of all sources that share a
+// sorted order (a.steps), and the time tiles of all sources that share a
 // direction are summed before any reflection tap is applied:
 //     sum_s y_s * g_{dir(s)} = sum_d g_d * (sum_{s: dir(s)=d} y_s)      (linearity)
 // so the TMEM window write and the 2 x nnz taps run once per *direction*
 // present in the group, not once per source.
 //
-// Pipeline: a producer warp streams each source's window tile (cp.async.bulk
-// with mbarrier completion) plus the two reflection rows of its direction into
-// a kMixStages-deep shared-memory ring.  The 4 consumer warps each add their
-// 624-sample slice of the tile into a warp-private accumulator, release the
-// stage, and on the last source of a direction write their lanes' windows into
-// their TMEM lane quarter and run both ears as one interleaved pair of
-// TMEM-load/FFMA chains.  Per-ear accumulators persist across the group and
-// leave once per item through a bulk store.
-constexpr int kMixStages = 6;
-constexpr int kMixThreads = kThreads + 32;  // 4 consumer warps + 1 TMA producer warp
-constexpr int kMixSlice = 32 * kR + 128;   // floats of the tile one warp needs (<= 512 + KWIN + 16)
+// Every warp is its own pipeline: lane 0 streams the warp's 624-sample slice
+// of each source tile (cp.async.bulk + mbarrier complete_tx) and, on a
+// direction's last source, its two reflection rows into a warp-private
+// kMixStages-deep ring, kMixStages-1 sources ahead; the warp adds slices into
+// a private accumulator and, per direction, writes its lanes' windows into its
+// TMEM lane quarter and runs both ears as one interleaved pair of
+// TMEM-load/FFMA chains.  No CTA-wide barrier in the steady state.  Per-ear
+// accumulators persist across the group and leave once per item (bulk store).
+constexpr int kMixStages = 3;
+constexpr int kMixSlice = 32 * kR + 112;  // floats of a tile one warp reads (KWIN <= 112)
 
 struct MixLayout {
-  int stage_floats, taps_off, meta_off, steps_off, staging_off, accum_off, bars_off, total;
+  int slice, stage_floats, taps_off, meta_off, warp_floats, accum_off, bars_off, total;
 };
 
 __host__ __device__ inline MixLayout mix_layout(int KWIN, int tap_stride) {
   MixLayout L{};
-  const int XH = KWIN + kR;
-  const int tile = (kW + XH + 31) & ~31;
-  const int slice = 32 * kR + XH;
-  L.taps_off = tile;                      // within a stage: [2 ears][tap_stride] int2
-  L.meta_off = tile + 4 * tap_stride;     // int4 {first, last, dir, src}
+  L.slice = 32 * kR + KWIN;                              // lane windows 16l + [0, 16 + KWIN)
+  L.taps_off = (L.slice + 3) & ~3;                        // [2 ears][tap_stride] int2
+  L.meta_off = L.taps_off + 4 * tap_stride;               // int4 {first, last, dir, src}
   L.stage_floats = (L.meta_off + 4 + 31) & ~31;
-  L.steps_off = kMixStages * L.stage_floats;             // int4 [src_per_group] producer step table
-  L.accum_off = L.steps_off + 4 * 256;                    // [warps][slice]
-  L.staging_off = L.accum_off + kWarps * ((slice + 31) & ~31);  // [warps][2 ears][512]
-  L.bars_off = L.staging_off + kWarps * 2 * 32 * kR;        // 2*kMixStages uint64
-  L.total = (L.bars_off + 4 * kMixStages) * 4 + 128;
+  L.accum_off = kMixStages * L.stage_floats;              // slice sums, then the item's store staging
+  L.warp_floats = L.accum_off + ((L.slice > 2 * 32 * kR ? L.slice : 2 * 32 * kR) + 31 & ~31);
+  L.bars_off = kWarps * L.warp_floats;                    // [warps][kMixStages] uint64
+  L.total = (L.bars_off + 2 * kWarps * kMixStages) * 4 + 128;
   return L;
 }
 
@@ -160,227 +158,222 @@ __device__ __forceinline__ int mix_group_size(const MixArgs& a, long long item) 
   return min(a.src_per_group, a.S - grp * a.src_per_group);
 }
 
-// Prefetch one (item, source) step into its ring stage (producer lane 0).
-// `ent` = {src, dir, first, last} from the host-built direction-sorted table.
-template <int KWIN>
-__device__ __forceinline__ void mix_issue(const MixArgs& a, const MixLayout& L, float* smem, uint64_t* full,
-                                          uint64_t* empty, int j, int4 ent, int issued) {
-  constexpr int XH = KWIN + kR;
-  const int stage = issued % kMixStages;
-  const unsigned par = (unsigned)((issued / kMixStages) & 1);
-  mbar_wait(&empty[stage], par ^ 1u);
-  const int src = ent.x, dir = ent.y, last = ent.w;
-  float* tile = smem + stage * L.stage_floats;
-  int2* taps = reinterpret_cast<int2*>(tile + L.taps_off);
-  const long long T0 = (long long)j * kW;
-  const long long w0 = T0 - XH;  // signal index of tile[0]
-  const long long lo = max(w0, 0LL), hi = min(T0 + kW, a.T);
-  const int n = (int)max(hi - lo, 0LL);
-  const int nb = n & ~3;
-  const unsigned tap_bytes = last ? 2u * a.tap_stride * 8u : 0u;
-  const float* y = a.y + (long long)src * a.y_pitch;
-  // zero fill / ragged remainder / metadata with generic stores, released by the arrive below
-  for (long long i = 0; i < lo - w0; ++i) tile[i] = 0.f;
-  for (int i = nb; i < n; ++i) tile[(lo - w0) + i] = __ldg(y + lo + i);
-  for (long long i = (lo - w0) + n; i < kW + XH; ++i) tile[i] = 0.f;
-  *reinterpret_cast<int4*>(tile + L.meta_off) = make_int4(ent.z, ent.w, dir, src);
-  mbar_arrive_expect_tx(&full[stage], (unsigned)nb * 4u + tap_bytes);
-  if (nb) bulk_load(tile + (lo - w0), y + lo, (unsigned)nb * 4u, &full[stage]);
-  if (last) {
-    for (int e = 0; e < 2; ++e) {
-      const int ee = e < a.ears ? e : 0;
-      bulk_load(taps + e * a.tap_stride, a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride,
-                (unsigned)a.tap_stride * 8u, &full[stage]);
-    }
-  }
-}
-
 template <int KWIN, int NNZT>
-__global__ void __maxnreg__(136) k_mix(MixArgs a) {
+__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) {
   constexpr int XH = KWIN + kR;
   constexpr int COLS = kR + KWIN;
-  constexpr int SLICE = 32 * kR + KWIN;  // tile floats one warp reads (lane windows 16l + [0, 128))
   extern __shared__ __align__(128) float smem[];
   __shared__ unsigned s_tbase;
   const MixLayout L = mix_layout(KWIN, a.tap_stride);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars_off);
-  uint64_t* empty = full + kMixStages;
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* wbase = smem + warp * L.warp_floats;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars_off) + warp * kMixStages;
+  float* acc_tile = wbase + L.accum_off;  // aliases the output staging `st`
+  float* st = acc_tile;
+
   if (warp == 0) tmem_alloc<COLS>(&s_tbase);
-  if (tid == 0) {
-    for (int i = 0; i < kMixStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kWarps);
-    }
+  if (lane == 0) {
+    for (int i = 0; i < kMixStages; ++i) mbar_init(&full[i], 1);
     mbar_fence_init();
   }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const unsigned tlane = s_tbase + ((unsigned)(32 * (warp & 3)) << 16);
+  const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
 
   const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
   const long long it0 = (long long)blockIdx.x * per;
   const long long it1 = min(a.n_items, it0 + per);
+  const int slice_sig0 = 32 * kR * warp - KWIN;  // signal offset of the slice relative to T0
 
-  if (warp == kWarps) {
-    // ---- producer warp: streams every (item, source) of this CTA into the ring;
-    //      the group's step table is staged in shared memory once per group
-    int4* s_steps = reinterpret_cast<int4*>(smem + L.steps_off);
-    int issued = 0, cur_grp = -1;
-    for (long long item = it0; item < it1; ++item) {
-      const int j = (int)(item % a.n_tiles);
-      const int grp = (int)(item / a.n_tiles);
-      const int ns = mix_group_size(a, item);
-      if (grp != cur_grp) {
-        __syncwarp();
-        for (int i = lane; i < ns; i += 32) s_steps[i] = a.steps[(long long)grp * a.src_per_group + i];
-        __syncwarp();
-        cur_grp = grp;
-      }
-      if (lane == 0)
-        for (int s = 0; s < ns; ++s, ++issued) mix_issue<KWIN>(a, L, smem, full, empty, j, s_steps[s], issued);
-      __syncwarp();
+  // ---- producer cursor (lane 0 issues; the warp shares step-table chunks) ----
+  long long p_item = it0;
+  int p_s = 0, issued = 0;
+  int4 ent_chunk = make_int4(0, 0, 0, 0);
+  long long chunk_item = -1;
+  int chunk_id = -1;
+  auto issue_one = [&]() {
+    // all 32 lanes call this (convergent), lane 0 issues
+    const int grp = (int)(p_item / a.n_tiles);
+    const int j = (int)(p_item % a.n_tiles);
+    const int cid = p_s >> 5;
+    if (p_item != chunk_item || cid != chunk_id) {
+      const int pos = grp * a.src_per_group + cid * 32 + lane;
+      const int ns = mix_group_size(a, p_item);
+      ent_chunk = (cid * 32 + lane < ns) ? a.steps[pos] : make_int4(0, 0, 0, 0);
+      chunk_item = p_item;
+      chunk_id = cid;
     }
-  } else {
-    int step = 0;
-    float* st = smem + L.staging_off + warp * 2 * 32 * kR;
-    float* acc_tile = smem + L.accum_off + warp * ((SLICE + 31) & ~31);
-    const int slice0 = (XH - KWIN) + 32 * kR * warp;  // this warp's first tile index
-    for (long long item = it0; item < it1; ++item) {
-      const int j = (int)(item % a.n_tiles);
-      const int grp = (int)(item / a.n_tiles);
-      const long long T0 = (long long)j * kW;
-      const int ns = mix_group_size(a, item);
-      float accA[16], accB[16];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        accA[r] = 0.f;
-        accB[r] = 0.f;
+    int4 ent;
+    ent.x = __shfl_sync(0xffffffffu, ent_chunk.x, p_s & 31);
+    ent.y = __shfl_sync(0xffffffffu, ent_chunk.y, p_s & 31);
+    ent.z = __shfl_sync(0xffffffffu, ent_chunk.z, p_s & 31);
+    ent.w = __shfl_sync(0xffffffffu, ent_chunk.w, p_s & 31);
+    if (lane == 0) {
+      const int stage = issued % kMixStages;
+      float* tile = wbase + stage * L.stage_floats;
+      int2* taps = reinterpret_cast<int2*>(tile + L.taps_off);
+      const int src = ent.x, dir = ent.y, last = ent.w;
+      const long long w0 = (long long)j * kW + slice_sig0;  // signal index of slice[0]
+      const long long lo = max(w0, 0LL), hi = min(w0 + L.slice, a.T);
+      const int n = (int)max(hi - lo, 0LL);
+      const int nb = n & ~3;
+      const float* y = a.y + (long long)src * a.y_pitch;
+      for (long long i = 0; i < lo - w0 && i < L.slice; ++i) tile[i] = 0.f;
+      for (int i = nb; i < n; ++i) tile[(lo - w0) + i] = __ldg(y + lo + i);
+      for (long long i = max(lo - w0, 0LL) + n; i < L.slice; ++i) tile[i] = 0.f;
+      *reinterpret_cast<int4*>(tile + L.meta_off) = make_int4(ent.z, ent.w, dir, src);
+      const unsigned tap_bytes = last ? 2u * a.tap_stride * 8u : 0u;
+      mbar_arrive_expect_tx(&full[stage], (unsigned)nb * 4u + tap_bytes);
+      if (nb) bulk_load(tile + (lo - w0), y + lo, (unsigned)nb * 4u, &full[stage]);
+      if (last) {
+        for (int e = 0; e < 2; ++e) {
+          const int ee = e < a.ears ? e : 0;
+          bulk_load(taps + e * a.tap_stride, a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride,
+                    (unsigned)a.tap_stride * 8u, &full[stage]);
+        }
       }
-      for (int s = 0; s < ns; ++s, ++step) {
-        const int stage = step % kMixStages;
-        mbar_wait(&full[stage], (unsigned)((step / kMixStages) & 1));
-        const float* tile = smem + stage * L.stage_floats;
-        const int4 meta = *reinterpret_cast<const int4*>(tile + L.meta_off);
-        // sum this direction's sources over the warp's slice (coalesced, conflict-free)
-        if (meta.x) {
-          for (int i = 4 * lane; i < SLICE; i += 128)
-            *reinterpret_cast<float4*>(&acc_tile[i]) = *reinterpret_cast<const float4*>(&tile[slice0 + i]);
-        } else {
-          for (int i = 4 * lane; i < SLICE; i += 128) {
-            float4 acc4 = *reinterpret_cast<const float4*>(&acc_tile[i]);
-            const float4 t4 = *reinterpret_cast<const float4*>(&tile[slice0 + i]);
-            acc4.x += t4.x;
-            acc4.y += t4.y;
-            acc4.z += t4.z;
-            acc4.w += t4.w;
-            *reinterpret_cast<float4*>(&acc_tile[i]) = acc4;
-          }
-        }
-        if (!meta.y) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
-          continue;
-        }
-        __syncwarp();
-        // lane windows -> TMEM (previous direction's loads were all waited)
-        {
-          const int wbase = 16 * lane;
+    }
+    ++issued;
+    if (++p_s >= mix_group_size(a, p_item)) {
+      p_s = 0;
+      ++p_item;
+    }
+  };
+  long long total = 0;
+  for (long long it = it0; it < it1; ++it) total += mix_group_size(a, it);
+  while (issued < min((long long)kMixStages - 1, total)) issue_one();
+
+  int step = 0;
+  for (long long item = it0; item < it1; ++item) {
+    const int j = (int)(item % a.n_tiles);
+    const int grp = (int)(item / a.n_tiles);
+    const long long T0 = (long long)j * kW;
+    const int ns = mix_group_size(a, item);
+    float accA[16], accB[16];
 #pragma unroll
-          for (int c = 0; c < COLS; c += 16) {
-            float v[16];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 t4 = *reinterpret_cast<const float4*>(&acc_tile[wbase + c + 4 * q]);
-              v[4 * q] = t4.x;
-              v[4 * q + 1] = t4.y;
-              v[4 * q + 2] = t4.z;
-              v[4 * q + 3] = t4.w;
-            }
-            tmem_st16(tlane + c, v);
-          }
-          tmem_wait_st();
-        }
-        const int2* tA = reinterpret_cast<const int2*>(tile + L.taps_off);
-        const int2* tB = tA + a.tap_stride;
-        const float keepB = a.ears > 1 ? 1.f : 0.f;
-        if constexpr (NNZT > 0) {
-          float XA0[16], XB0[16], XA1[16], XB1[16];
-          int2 ta = tA[0], tb = tB[0];
-          int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
-          tmem_ld16(XA0, tlane + ta.x);
-          tmem_ld16(XB0, tlane + tb.x);
-#pragma unroll
-          for (int k = 0; k < NNZT; ++k) {
-            const int2 tann = tA[k + 2 < NNZT ? k + 2 : NNZT - 1];
-            const int2 tbnn = tB[k + 2 < NNZT ? k + 2 : NNZT - 1];
-            float(&XA)[16] = (k & 1) ? XA1 : XA0;
-            float(&XB)[16] = (k & 1) ? XB1 : XB0;
-            float(&YA)[16] = (k & 1) ? XA0 : XA1;
-            float(&YB)[16] = (k & 1) ? XB0 : XB1;
-            const unsigned na = tlane + tan.x, nb = tlane + tbn.x;
-            tmem_wait_ld();
-            if (k + 1 < NNZT) {
-              tmem_ld16(YA, na);
-              tmem_ld16(YB, nb);
-            }
-            const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-              accA[r] = fmaf(va, XA[r], accA[r]);
-              accB[r] = fmaf(vb, XB[r], accB[r]);
-            }
-            ta = tan;
-            tb = tbn;
-            tan = tann;
-            tbn = tbnn;
-          }
-        } else {
-          const int dir = meta.z;
-          const int nA = a.row_nnz[dir];
-          const int nB = a.ears > 1 ? a.row_nnz[a.dirs + dir] : 0;
-          const int nk = max(nA, nB);
-          for (int k = 0; k < nk; ++k) {
-            const int2 ta = tA[k], tb = tB[k];
-            float XA[16], XB[16];
-            tmem_ld16(XA, tlane + ta.x);
-            tmem_ld16(XB, tlane + tb.x);
-            tmem_wait_ld();
-            const float va = k < nA ? __int_as_float(ta.y) : 0.f;
-            const float vb = k < nB ? __int_as_float(tb.y) : 0.f;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-              accA[r] = fmaf(va, XA[r], accA[r]);
-              accB[r] = fmaf(vb, XB[r], accB[r]);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
-      }
-      // ---- the group's partial for this tile -----------------------------
-      const long long out_col = T0 + (long long)warp * 32 * kR;
-      if (out_col < a.zlen) {
+    for (int r = 0; r < 16; ++r) {
+      accA[r] = 0.f;
+      accB[r] = 0.f;
+    }
+    for (int s = 0; s < ns; ++s, ++step) {
+      if (issued < total) issue_one();  // refills the stage this warp released last step
+      const int stage = step % kMixStages;
+      mbar_wait(&full[stage], (unsigned)((step / kMixStages) & 1));
+      const float* tile = wbase + stage * L.stage_floats;
+      const int4 meta = *reinterpret_cast<const int4*>(tile + L.meta_off);
+      if (s == 0) {  // the previous item's bulk store may still be reading acc_tile
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
-#pragma unroll
-        for (int r = 0; r < 16; r += 4) {
-          *reinterpret_cast<float4*>(&st[lane * 16 + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
-          *reinterpret_cast<float4*>(&st[512 + lane * 16 + r]) =
-              make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          for (int e = 0; e < a.ears; ++e)
-            bulk_store(a.part + ((long long)grp * a.ears + e) * a.part_pitch + out_col, st + 512 * e, 32 * kR * 4);
+      }
+      // sum this direction's sources over the warp's slice (coalesced, conflict-free)
+      if (meta.x) {
+        for (int i = 4 * lane; i < L.slice; i += 128)
+          *reinterpret_cast<float4*>(&acc_tile[i]) = *reinterpret_cast<const float4*>(&tile[i]);
+      } else {
+        for (int i = 4 * lane; i < L.slice; i += 128) {
+          float4 acc4 = *reinterpret_cast<const float4*>(&acc_tile[i]);
+          const float4 t4 = *reinterpret_cast<const float4*>(&tile[i]);
+          acc4.x += t4.x;
+          acc4.y += t4.y;
+          acc4.z += t4.z;
+          acc4.w += t4.w;
+          *reinterpret_cast<float4*>(&acc_tile[i]) = acc4;
         }
       }
+      __syncwarp();
+      if (!meta.y) continue;
+      // lane windows -> TMEM (previous direction's loads were all waited)
+      {
+#pragma unroll
+        for (int c = 0; c < COLS; c += 16) {
+          float v[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 t4 = *reinterpret_cast<const float4*>(&acc_tile[16 * lane + c + 4 * q]);
+            v[4 * q] = t4.x;
+            v[4 * q + 1] = t4.y;
+            v[4 * q + 2] = t4.z;
+            v[4 * q + 3] = t4.w;
+          }
+          tmem_st16(tlane + c, v);
+        }
+        tmem_wait_st();
+      }
+      const int2* tA = reinterpret_cast<const int2*>(tile + L.taps_off);
+      const int2* tB = tA + a.tap_stride;
+      const float keepB = a.ears > 1 ? 1.f : 0.f;
+      if constexpr (NNZT > 0) {
+        float XA0[16], XB0[16], XA1[16], XB1[16];
+        int2 ta = tA[0], tb = tB[0];
+        int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
+        tmem_ld16(XA0, tlane + ta.x);
+        tmem_ld16(XB0, tlane + tb.x);
+#pragma unroll
+        for (int k = 0; k < NNZT; ++k) {
+          const int2 tann = tA[k + 2 < NNZT ? k + 2 : NNZT - 1];
+          const int2 tbnn = tB[k + 2 < NNZT ? k + 2 : NNZT - 1];
+          float(&XA)[16] = (k & 1) ? XA1 : XA0;
+          float(&XB)[16] = (k & 1) ? XB1 : XB0;
+          float(&YA)[16] = (k & 1) ? XA0 : XA1;
+          float(&YB)[16] = (k & 1) ? XB0 : XB1;
+          const unsigned na = tlane + tan.x, nb = tlane + tbn.x;
+          tmem_wait_ld();
+          if (k + 1 < NNZT) {
+            tmem_ld16(YA, na);
+            tmem_ld16(YB, nb);
+          }
+          const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            accA[r] = fmaf(va, XA[r], accA[r]);
+            accB[r] = fmaf(vb, XB[r], accB[r]);
+          }
+          ta = tan;
+          tb = tbn;
+          tan = tann;
+          tbn = tbnn;
+        }
+      } else {
+        const int dir = meta.z;
+        const int nA = a.row_nnz[dir];
+        const int nB = a.ears > 1 ? a.row_nnz[a.dirs + dir] : 0;
+        const int nk = max(nA, nB);
+        for (int k = 0; k < nk; ++k) {
+          const int2 ta = tA[k], tb = tB[k];
+          float XA[16], XB[16];
+          tmem_ld16(XA, tlane + ta.x);
+          tmem_ld16(XB, tlane + tb.x);
+          tmem_wait_ld();
+          const float va = k < nA ? __int_as_float(ta.y) : 0.f;
+          const float vb = k < nB ? __int_as_float(tb.y) : 0.f;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            accA[r] = fmaf(va, XA[r], accA[r]);
+            accB[r] = fmaf(vb, XB[r], accB[r]);
+          }
+        }
+      }
+      __syncwarp();
     }
-    if (lane == 0) bulk_wait_all();
-  }  // consumer warps
+    // ---- the group's partial for this tile -------------------------------
+    const long long out_col = T0 + (long long)warp * 32 * kR;
+    if (out_col < a.zlen) {
+#pragma unroll
+      for (int r = 0; r < 16; r += 4) {
+        *reinterpret_cast<float4*>(&st[lane * 16 + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
+        *reinterpret_cast<float4*>(&st[512 + lane * 16 + r]) =
+            make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int e = 0; e < a.ears; ++e)
+          bulk_store(a.part + ((long long)grp * a.ears + e) * a.part_pitch + out_col, st + 512 * e, 32 * kR * 4);
+      }
+    }
+  }
+  if (lane == 0) bulk_wait_all();
   tmem_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<COLS>(s_tbase);
@@ -389,14 +382,17 @@ __global__ void __maxnreg__(136) k_mix(MixArgs a) {
 template <int KWIN, int NNZT>
 static cudaError_t launch_mix_t(const MixArgs& a, int sm_count, cudaStream_t st) {
   const int bytes = mix_layout(KWIN, a.tap_stride).total;
-  auto kern = k_mix<KWIN, NNZT>;
+  auto kern = k_mix<KWIN, NNZT>;  // 4 warps, one TMEM lane quarter each
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
-  const int per_sm = std::min(3, 512 / (kR + KWIN));
+  // TMEM bounds co-residency (512 / COLS CTAs per SM); shared memory and
+  // registers are sized to allow exactly that many.
+  int per_sm = 512 / (kR + KWIN);
+  if (getenv("TOEP_MIX_PERSM")) per_sm = atoi(getenv("TOEP_MIX_PERSM"));
   long long grid = (long long)sm_count * per_sm;
   if (grid > a.n_items) grid = a.n_items;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kMixThreads, bytes, st>>>(a);
+  kern<<<(unsigned)grid, kThreads, bytes, st>>>(a);
   return cudaGetLastError();
 }
 

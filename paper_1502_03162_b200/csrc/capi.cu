@@ -457,6 +457,15 @@ struct toep_mixer {
   std::vector<int> h_dir;
   int4* d_steps = nullptr;      // direction-sorted step table of the last [s0, s0+count) range
   int order_s0 = -1, order_count = -1;
+  // same-direction buckets of that range (used when some direction has > 1 source)
+  int buckets = 0;
+  bool use_buckets = false;
+  int* d_bsrc = nullptr;        // sources sorted by direction
+  int* d_bptr = nullptr;        // bucket b = d_bsrc[d_bptr[b] .. d_bptr[b+1])
+  int4* d_bsteps = nullptr;     // one step per bucket {b, dir, 1, 1}
+  float* d_yb = nullptr;        // bucket sums [buckets][yb_pitch]
+  size_t yb_bytes = 0;
+  long long yb_pitch = 0;
   float* d_part = nullptr;
   size_t part_bytes = 0;
 };
@@ -486,6 +495,9 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
   m->h_dir.assign(src_dir_host, src_dir_host + n_src);
   cudaError_t e = cudaMalloc(&m->d_dir, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_steps, n_src * sizeof(int4));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_bsrc, n_src * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_bptr, (n_src + 1) * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_bsteps, n_src * sizeof(int4));
   if (e == cudaSuccess) e = cudaMemcpy(m->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     toep_mixer_destroy(m);
@@ -499,6 +511,10 @@ int toep_mixer_destroy(toep_mixer* m) {
   if (!m) return TOEP_OK;
   if (m->d_dir) cudaFree(m->d_dir);
   if (m->d_steps) cudaFree(m->d_steps);
+  if (m->d_bsrc) cudaFree(m->d_bsrc);
+  if (m->d_bptr) cudaFree(m->d_bptr);
+  if (m->d_bsteps) cudaFree(m->d_bsteps);
+  if (m->d_yb) cudaFree(m->d_yb);
   if (m->d_part) cudaFree(m->d_part);
   delete m;
   return TOEP_OK;
@@ -518,7 +534,64 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   if (m->r->ears > 1 && z_pitch < m->zlen) return fail(TOEP_ERR_INVALID, "z pitch too small");
   cudaStream_t st = S(stream);
   const toep_taps* g = m->r->g;
-  const int groups = (count + kSrcPerGroup - 1) / kSrcPerGroup;
+  if (s0 != m->order_s0 || count != m->order_count) {
+    // stable sort of the range by direction; per sorted position {src, dir, first, last}
+    // within its group: sources sharing a direction are summed before their taps
+    std::vector<int> ord(count);
+    for (int i = 0; i < count; ++i) ord[i] = i;
+    const int* dir = m->h_dir.data() + s0;
+    std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
+    std::vector<int4> steps(count);
+    std::vector<int> bptr(1, 0);
+    std::vector<int4> bsteps;
+    for (int p = 0; p < count; ++p) {
+      const int d = dir[ord[p]];
+      const bool first = (p % kSrcPerGroup == 0) || dir[ord[p - 1]] != d;
+      const bool last = ((p + 1) % kSrcPerGroup == 0) || p + 1 == count || dir[ord[p + 1]] != d;
+      steps[p] = make_int4(ord[p], d, first ? 1 : 0, last ? 1 : 0);
+      if (p + 1 == count || dir[ord[p + 1]] != d) {
+        bsteps.push_back(make_int4((int)bsteps.size(), d, 1, 1));
+        bptr.push_back(p + 1);
+      }
+    }
+    m->buckets = (int)bsteps.size();
+    m->use_buckets = m->buckets < count;  // some direction holds several sources
+    TOEP_CUDA(cudaMemcpyAsync(m->d_steps, steps.data(), count * sizeof(int4), cudaMemcpyHostToDevice, st));
+    TOEP_CUDA(cudaMemcpyAsync(m->d_bsrc, ord.data(), count * sizeof(int), cudaMemcpyHostToDevice, st));
+    TOEP_CUDA(cudaMemcpyAsync(m->d_bptr, bptr.data(), bptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    TOEP_CUDA(cudaMemcpyAsync(m->d_bsteps, bsteps.data(), bsteps.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    TOEP_CUDA(cudaStreamSynchronize(st));
+    m->order_s0 = s0;
+    m->order_count = count;
+  }
+  // sources -> per-direction sums (one HBM streaming pass) when directions repeat
+  const float* xs = y;
+  long long xs_pitch = y_pitch;
+  int nsteps = count;
+  const int4* steps_dev = m->d_steps;
+  if (m->use_buckets) {
+    const long long pitch = round_up(m->T, 4);
+    const size_t need_b = (size_t)m->buckets * pitch * sizeof(float);
+    if (need_b > m->yb_bytes) {
+      if (m->d_yb) {
+        TOEP_CUDA(cudaStreamSynchronize(st));
+        cudaFree(m->d_yb);
+        m->d_yb = nullptr;
+        m->yb_bytes = 0;
+      }
+      TOEP_CUDA(cudaMalloc(&m->d_yb, need_b));
+      m->yb_bytes = need_b;
+    }
+    m->yb_pitch = pitch;
+    cudaError_t eb = launch_bucket_sum(y, count > 1 ? y_pitch : round_up(m->T, 4), m->T, m->d_bsrc, m->d_bptr,
+                                       m->buckets, m->d_yb, pitch, sm_count_cached(), st);
+    if (eb != cudaSuccess) return cuda_fail(eb, "launch_bucket_sum");
+    xs = m->d_yb;
+    xs_pitch = pitch;
+    nsteps = m->buckets;
+    steps_dev = m->d_bsteps;
+  }
+  const int groups = (nsteps + kSrcPerGroup - 1) / kSrcPerGroup;
   const int n_tiles = (int)((m->zlen + kW - 1) / kW);
   const long long part_pitch = (long long)n_tiles * kW;
   const size_t need = (size_t)groups * m->r->ears * part_pitch * sizeof(float);
@@ -532,32 +605,13 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     TOEP_CUDA(cudaMalloc(&m->d_part, need));
     m->part_bytes = need;
   }
-  if (s0 != m->order_s0 || count != m->order_count) {
-    // stable sort of the range by direction; per sorted position {src, dir, first, last}
-    // within its group: sources sharing a direction are summed before their taps
-    std::vector<int> ord(count);
-    for (int i = 0; i < count; ++i) ord[i] = i;
-    const int* dir = m->h_dir.data() + s0;
-    std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
-    std::vector<int4> steps(count);
-    for (int p = 0; p < count; ++p) {
-      const int d = dir[ord[p]];
-      const bool first = (p % kSrcPerGroup == 0) || dir[ord[p - 1]] != d;
-      const bool last = ((p + 1) % kSrcPerGroup == 0) || p + 1 == count || dir[ord[p + 1]] != d;
-      steps[p] = make_int4(ord[p], d, first ? 1 : 0, last ? 1 : 0);
-    }
-    TOEP_CUDA(cudaMemcpyAsync(m->d_steps, steps.data(), count * sizeof(int4), cudaMemcpyHostToDevice, st));
-    TOEP_CUDA(cudaStreamSynchronize(st));
-    m->order_s0 = s0;
-    m->order_count = count;
-  }
   MixArgs a{};
-  a.y = y;
-  a.steps = m->d_steps;
+  a.y = xs;
+  a.steps = steps_dev;
   a.T = m->T;
-  a.y_pitch = y_pitch;
+  a.y_pitch = xs_pitch;
   a.src_dir = m->d_dir + s0;
-  a.S = count;
+  a.S = nsteps;
   a.taps = g->d_kw;
   a.row_nnz = g->d_nnz;
   a.tap_stride = g->tap_stride;

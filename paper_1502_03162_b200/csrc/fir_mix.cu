@@ -266,8 +266,11 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
       }
-      // sum this direction's sources over the warp's slice (coalesced, conflict-free)
-      if (meta.x) {
+      // sum this direction's sources over the warp's slice (coalesced, conflict-free);
+      // a direction with a single source reads its window straight from the stage
+      const float* win = (meta.x && meta.y) ? tile : acc_tile;
+      if (meta.x && meta.y) {
+      } else if (meta.x) {
         for (int i = 4 * lane; i < L.slice; i += 128)
           *reinterpret_cast<float4*>(&acc_tile[i]) = *reinterpret_cast<const float4*>(&tile[i]);
       } else {
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
           float v[16];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 t4 = *reinterpret_cast<const float4*>(&acc_tile[16 * lane + c + 4 * q]);
+            const float4 t4 = *reinterpret_cast<const float4*>(&win[16 * lane + c + 4 * q]);
             v[4 * q] = t4.x;
             v[4 * q + 1] = t4.y;
             v[4 * q + 2] = t4.z;
@@ -417,6 +420,60 @@ cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st
     case 496: return mix_nnz<496>(a, sm_count, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------ same-direction source sums ----
+// yb[b][t] = sum over the sources of bucket b (all at one direction) of y_s[t].
+// Pure streaming pass (HBM-bound): float4 loads, up to 4 sources in flight.
+__global__ void __launch_bounds__(256) k_bucket_sum(const float* __restrict__ y, long long y_pitch, long long T,
+                                                    const int* __restrict__ bsrc, const int* __restrict__ bptr,
+                                                    float* __restrict__ yb, long long yb_pitch) {
+  const int b = blockIdx.y;
+  const int i0 = bptr[b], i1 = bptr[b + 1];
+  float* out = yb + (long long)b * yb_pitch;
+  const long long n4 = T >> 2;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (long long)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int i = i0;
+    for (; i + 4 <= i1; i += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(y + (long long)bsrc[i + u] * y_pitch) + q);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+    for (; i < i1; ++i) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(y + (long long)bsrc[i] * y_pitch) + q);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(out)[q] = acc;
+  }
+  if (blockIdx.x == 0) {
+    for (long long t = 4 * n4 + threadIdx.x; t < T; t += blockDim.x) {
+      float acc = 0.f;
+      for (int i = i0; i < i1; ++i) acc += y[(long long)bsrc[i] * y_pitch + t];
+      out[t] = acc;
+    }
+  }
+}
+
+cudaError_t launch_bucket_sum(const float* y, long long y_pitch, long long T, const int* bsrc, const int* bptr,
+                              int buckets, float* yb, long long yb_pitch, int sm_count, cudaStream_t st) {
+  const long long n4 = T >> 2;
+  long long bx = (n4 + 255) / 256;
+  const long long cap = std::max(1LL, (long long)sm_count * 8 / std::max(1, buckets) + 1);
+  if (bx > cap * 64) bx = cap * 64;
+  if (bx < 1) bx = 1;
+  k_bucket_sum<<<dim3((unsigned)bx, (unsigned)buckets), 256, 0, st>>>(y, y_pitch, T, bsrc, bptr, yb, yb_pitch);
+  return cudaGetLastError();
 }
 
 __global__ void k_mix_reduce(const float* __restrict__ part, int groups, int ears, long long part_pitch,

@@ -108,6 +108,10 @@ struct MixArgs {
 };
 cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st);
 
+// yb[b] = sum of the sources bsrc[bptr[b] .. bptr[b+1]) (all of one direction).
+cudaError_t launch_bucket_sum(const float* y, long long y_pitch, long long T, const int* bsrc, const int* bptr,
+                              int buckets, float* yb, long long yb_pitch, int sm_count, cudaStream_t st);
+
 // z[e][t] = sum_g part[g][e][t]  (fixed order, fp32)
 cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long part_pitch, long long zlen,
                               float* z, long long z_pitch, cudaStream_t st);

@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
   using C = RenderCfg<KWIN>;
   extern __shared__ float smem_raw[];
   __shared__ unsigned s_tbase;
-  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-align the dynamic base by pointer arithmetic on the shared array (keeps the
+  // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
+  float* smem = smem_raw + (((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) >> 2);
 
   const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.dirs_per_group, a.tap_stride);
   float* s_x = smem + L.x_off;

@@ -63,6 +63,20 @@ __device__ __forceinline__ void tmem_st16(unsigned ta, const float (&d)[16]) {
       : "memory");
 }
 
+// One lane of the (converged) warp; lets ptxas issue uniform-datapath ops
+// (UTMA*/UBLKCP) without a per-lane serialisation loop.
+__device__ __forceinline__ bool elect_one() {
+  unsigned pred;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ------------------------------------------------------- bulk (TMA) ops ----
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

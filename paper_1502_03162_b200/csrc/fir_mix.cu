@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
+      if (elect_one()) {
         for (int e = 0; e < a.ears; ++e)
           bulk_store(a.part + ((long long)grp * a.ears + e) * a.part_pitch + out_col, st + 512 * e, 32 * kR * 4);
       }

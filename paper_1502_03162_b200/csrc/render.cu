@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
       if (pp == 1 || p + 1 == p1) {
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if (elect_one()) {
           for (int q = 0; q <= pp; ++q) {
             const int pq = p - pp + q;
             const int rowA = e * a.dirs + dbeg + 2 * pq;

@@ -188,30 +188,41 @@ int toep_taps_info(const toep_taps* t, int32_t* rows, int32_t* length, int32_t* 
 }  // extern "C"
 
 // Stage-2 ("reflection") launch over `nrows` consecutive rows of a table,
-// all reading the same input signal x (nx samples).
-static int reflect_rows(const toep_taps* t, int row0, int nrows, const float* x, long long nx, float* out,
-                        long long out_pitch, cudaStream_t st) {
+// all reading the same input signal x (nx samples).  `pairs`/`pnnz` are the
+// rows' pair-interleaved taps (k_pair_taps); null -> built here for this call.
+static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pairs, const int4* pnnz, const float* x,
+                        long long nx, float* out, long long out_pitch, cudaStream_t st) {
   const long long out_len = nx + t->length - 1;
   if (t->kwin > 0) {
     if (!aligned16(out) || (nrows > 1 && out_pitch % 4 != 0))
       return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");
+    const int P = (nrows + 1) / 2;
+    int4* tmp = nullptr;
+    if (!pairs) {
+      TOEP_CUDA(cudaMallocAsync(&tmp, (size_t)P * (t->tap_stride + 1) * sizeof(int4), st));
+      cudaError_t ep = launch_pair_taps(t->d_kw + (size_t)row0 * t->tap_stride, t->d_nnz + row0, 1, nrows,
+                                        t->tap_stride, t->kwin, tmp, tmp + (size_t)P * t->tap_stride, st);
+      if (ep != cudaSuccess) {
+        cudaFreeAsync(tmp, st);
+        return cuda_fail(ep, "launch_pair_taps");
+      }
+      pairs = tmp;
+      pnnz = tmp + (size_t)P * t->tap_stride;
+    }
     RenderArgs a{};
     a.x = x;
     a.nx = nx;
     a.x_pitch = 0;
     a.f = nullptr;
     a.lf_pad = 0;
-    a.taps = t->d_kw + (size_t)row0 * t->tap_stride;
-    a.row_nnz = t->d_nnz + row0;
+    a.pairs = pairs;
+    a.pair_nnz = pnnz;
+    a.pairs_per_ear = P;
     a.tap_stride = t->tap_stride;
     a.uniform_nnz = t->uniform;
     a.tap_stride_nnz = t->max_nnz;
     a.dirs = nrows;
     a.ears = 1;
-    const int budget_taps = 2048;  // int2 entries staged per group (16 KB)
-    const int dpg_max = std::max(1, std::min(nrows, budget_taps / t->tap_stride));
-    a.groups = (nrows + dpg_max - 1) / dpg_max;
-    a.dirs_per_group = (nrows + a.groups - 1) / a.groups;  // group sizes are q or q+1
     a.n_tiles = (int)((out_len + kW - 1) / kW);
     a.n_items = (long long)nrows * a.n_tiles;  // work units (direction x tile)
     a.out = out;
@@ -219,8 +230,8 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const float* x,
     a.out_len = out_len;
     RenderMaps maps;
     cudaError_t e = make_render_maps(out, nrows, out_len, out_pitch, &maps);
-    if (e != cudaSuccess) return cuda_fail(e, "tensor map (output rows)");
-    e = launch_render(a, maps, t->kwin, false, sm_count_cached(), st);
+    if (e == cudaSuccess) e = launch_render(a, maps, t->kwin, false, sm_count_cached(), st);
+    if (tmp) cudaFreeAsync(tmp, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_render(stage 2)");
     return TOEP_OK;
   }
@@ -265,7 +276,7 @@ int toep_taps_conv(const toep_taps* t, int32_t row, const float* y, int64_t ny, 
   if (!t) return fail(TOEP_ERR_INVALID, "null table");
   if (row < 0 || row >= t->rows) return fail(TOEP_ERR_INVALID, "row %d out of range", row);
   if (ny < 1 || !y || !out) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
-  return reflect_rows(t, row, 1, y, ny, out, 0, S(stream));
+  return reflect_rows(t, row, 1, nullptr, nullptr, y, ny, out, 0, S(stream));
 }
 
 int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps, float* out, int64_t* macs,
@@ -297,7 +308,7 @@ int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const f
   toep_taps* t = nullptr;
   int rc = taps_build(1, (int32_t)length, row_ptr, indices, values, true, st, &t);
   if (rc != TOEP_OK) return rc;
-  rc = reflect_rows(t, 0, 1, y, ny, out, 0, st);
+  rc = reflect_rows(t, 0, 1, nullptr, nullptr, y, ny, out, 0, st);
   toep_taps_destroy(t);
   if (rc == TOEP_OK && macs) *macs = nnz * ny;  // _kernels.pyx:43
   return rc;
@@ -307,20 +318,12 @@ int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const f
 
 // -------------------------------------------------------------- renderer ----
 struct toep_renderer {
-  int ears = 0, lf = 0, lf_pad = 0, dirs = 0;
+  int ears = 0, lf = 0, lf_pad = 0, dirs = 0, pairs_per_ear = 0;
   const toep_taps* g = nullptr;
-  float* d_f = nullptr;  // [ears][lf_pad]
+  float* d_f = nullptr;      // [ears][lf_pad]
+  int4* d_pairs = nullptr;   // [ears][pairs_per_ear][tap_stride] pair-interleaved taps (k_render)
+  int4* d_pnnz = nullptr;    // [ears][pairs_per_ear]
 };
-
-static int render_dirs_per_group(const toep_renderer* r) {
-  // keep the CTA's shared memory inside its 1/(512/COLS) share of the SM
-  const int kwin = r->g->kwin;
-  const int per_sm = 512 / (kR + kwin);
-  const int budget = 227 * 1024 / per_sm - 1024;
-  int dpg = std::min(r->dirs, std::max(1, 2048 / r->g->tap_stride));
-  while (dpg > 1 && (int)render_smem_bytes(kwin, true, r->lf_pad, dpg, r->g->tap_stride) > budget) dpg = (dpg + 1) / 2;
-  return dpg;
-}
 
 extern "C" {
 
@@ -347,6 +350,15 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
     for (int j = 0; j < lf; ++j) fp[(size_t)e * r->lf_pad + j] = f_host[(size_t)e * lf + j];
   cudaError_t e = cudaMalloc(&r->d_f, fp.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMemcpy(r->d_f, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (g->kwin > 0) {
+    r->pairs_per_ear = (dirs + 1) / 2;
+    const size_t np = (size_t)ears * r->pairs_per_ear;
+    if (e == cudaSuccess) e = cudaMalloc(&r->d_pairs, np * g->tap_stride * sizeof(int4));
+    if (e == cudaSuccess) e = cudaMalloc(&r->d_pnnz, np * sizeof(int4));
+    if (e == cudaSuccess)
+      e = launch_pair_taps(g->d_kw, g->d_nnz, ears, dirs, g->tap_stride, g->kwin, r->d_pairs, r->d_pnnz, nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
   if (e != cudaSuccess) {
     toep_renderer_destroy(r);
     return cuda_fail(e, "toep_renderer_create");
@@ -358,6 +370,8 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
 int toep_renderer_destroy(toep_renderer* r) {
   if (!r) return TOEP_OK;
   if (r->d_f) cudaFree(r->d_f);
+  if (r->d_pairs) cudaFree(r->d_pairs);
+  if (r->d_pnnz) cudaFree(r->d_pnnz);
   delete r;
   return TOEP_OK;
 }
@@ -387,16 +401,14 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.nx = ny;
     a.f = r->d_f;
     a.lf_pad = r->lf_pad;
-    a.taps = g->d_kw;
-    a.row_nnz = g->d_nnz;
+    a.pairs = r->d_pairs;
+    a.pair_nnz = r->d_pnnz;
+    a.pairs_per_ear = r->pairs_per_ear;
     a.tap_stride = g->tap_stride;
     a.uniform_nnz = g->uniform;
     a.tap_stride_nnz = g->max_nnz;
     a.dirs = r->dirs;
     a.ears = r->ears;
-    const int dpg_max = render_dirs_per_group(r);
-    a.groups = (r->dirs + dpg_max - 1) / dpg_max;
-    a.dirs_per_group = (r->dirs + a.groups - 1) / a.groups;  // group sizes are q or q+1
     a.n_tiles = (int)((out_len + kW - 1) / kW);
     a.n_items = (long long)a.ears * a.dirs * a.n_tiles;  // work units (direction x tile)
     a.out = out;
@@ -443,7 +455,9 @@ int toep_renderer_reflect(const toep_renderer* r, int32_t ear, const float* yf, 
   if (ear < 0 || ear >= r->ears) return fail(TOEP_ERR_INVALID, "ear %d out of range", ear);
   if (nyf < 1 || !yf || !out) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
   if (r->dirs > 1 && out_pitch < nyf + r->g->length - 1) return fail(TOEP_ERR_INVALID, "output pitch too small");
-  return reflect_rows(r->g, ear * r->dirs, r->dirs, yf, nyf, out, out_pitch, S(stream));
+  const int4* pairs = r->d_pairs ? r->d_pairs + (size_t)ear * r->pairs_per_ear * r->g->tap_stride : nullptr;
+  const int4* pnnz = r->d_pnnz ? r->d_pnnz + (size_t)ear * r->pairs_per_ear : nullptr;
+  return reflect_rows(r->g, ear * r->dirs, r->dirs, pairs, pnnz, yf, nyf, out, out_pitch, S(stream));
 }
 
 }  // extern "C"

@@ -21,15 +21,14 @@ struct RenderArgs {
   long long x_pitch;     // per-ear input stride (stage-2-only mode)
   const float* f;        // [ears][lf_pad] resonance taps, zero padded (stage1)
   int lf_pad;            // multiple of 16
-  const int2* taps;      // [ears*dirs][tap_stride]
-  const int* row_nnz;    // [ears*dirs]
-  int tap_stride;        // entries per row (>= max nnz)
+  const int4* pairs;     // [ears][pairs_per_ear][tap_stride] {colA, vA, colB, vB} (k_pair_taps)
+  const int4* pair_nnz;  // [ears][pairs_per_ear] {nnzA, nnzB, 0, 0}
+  int pairs_per_ear;     // ceil(dirs / 2)
+  int tap_stride;        // entries per row (>= max nnz, even)
   int uniform_nnz;       // 1 if every row holds exactly tap_stride_nnz taps
   int tap_stride_nnz;
   int dirs;              // directions per ear
   int ears;
-  int dirs_per_group;
-  int groups;            // ceil(dirs / dirs_per_group)
   int n_tiles;           // ceil(out_len / 2048)
   long long n_items;     // work units: ears * dirs * n_tiles
   float* out;            // row r at out + r * out_pitch
@@ -45,7 +44,9 @@ struct RenderMaps {
 };
 
 int render_kwin_for(int K);
-size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int dpg, int tap_stride);
+size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int tap_stride);
+cudaError_t launch_pair_taps(const int2* rows, const int* nnz, int n_seg, int seg, int stride, int kwin, int4* out,
+                             int4* out_nnz, cudaStream_t st);
 cudaError_t make_render_maps(float* out, long long rows, long long out_len, long long out_pitch, RenderMaps* m);
 cudaError_t launch_render(const RenderArgs& a, const RenderMaps& m, int kwin, bool stage1, int sm_count,
                           cudaStream_t st);

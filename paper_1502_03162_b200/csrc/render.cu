@@ -17,6 +17,8 @@
 //     TMEM lane row once per tile; every sparse tap (runtime offset o, weight v)
 //     then costs one tcgen05.ld.32x32b.x16 at column KWIN-o plus 16 FFMA.
 //   * each warp's 512 outputs per row leave through a cp.async.bulk store.
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -35,22 +37,22 @@ struct RenderCfg {
 };
 
 struct SmemLayout {
-  int region_off, x_off, yf_off, halo_off, f_off, taps_off, nnz_off, total;
+  int region_off, x_off, yf_off, halo_off, f_off, ring_off, nnz_off, bars_off, chunk_pairs, total;
 };
 
 constexpr int kStageFloatsPerWarp = 4 * 32 * kR;  // 4 directions x 512 outputs
+constexpr int kTapRing = 3;                        // tap-chunk buffers streamed by TMA
 
 // Shared memory plan.  The stage-1 input tile (s_x) and the y*f tile (s_yf)
 // are only live between an item's start and its TMEM window write, the bulk
 // store staging only during its direction loop, so they share one region.
-// Tap tables are staged per (ear, group) as direction *pairs*: entry
-// [pair][k] = int4 {colA, vA, colB, vB}, so one LDS.128 feeds two
-// independent TMEM-load/FFMA chains.
-__host__ __device__ inline SmemLayout render_smem_layout(int KWIN, bool stage1, int lf_pad, int dpg,
-                                                         int tap_stride) {
+// Reflection taps are not staged per direction group: chunks of direction
+// pairs (int4 {colA, vA, colB, vB} per tap, host-interleaved) stream through a
+// kTapRing-deep ring by cp.async.bulk, so one work item covers every
+// direction of an ear for its time tile.
+__host__ __device__ inline SmemLayout render_smem_layout(int KWIN, bool stage1, int lf_pad, int tap_stride) {
   SmemLayout L{};
   const int YH = KWIN + kR;
-  const int pairs = (dpg + 1) / 2;
   L.region_off = 0;
   L.x_off = 0;
   int tile = stage1 ? ((padded_len(kW + YH + lf_pad) + 31) & ~31) : 0;
@@ -62,47 +64,38 @@ __host__ __device__ inline SmemLayout render_smem_layout(int KWIN, bool stage1, 
   off += (YH + 31) & ~31;
   L.f_off = off;
   off += (lf_pad + 31) & ~31;
-  L.taps_off = off;  // int4 entries -> 4 floats each
-  off += 4 * pairs * tap_stride;
-  L.nnz_off = off;
-  off += 2 * pairs;
+  int cp = 4096 / (tap_stride * 16);  // pairs per chunk: ~4 KB chunks
+  if (cp < 1) cp = 1;
+  if (cp > 32) cp = 32;
+  L.chunk_pairs = cp;
+  L.ring_off = off;  // [kTapRing][cp][tap_stride] int4
+  off += kTapRing * cp * tap_stride * 4;
+  L.nnz_off = off;  // [kTapRing][cp] int4 {nnzA, nnzB, 0, 0}
+  off += kTapRing * cp * 4;
+  L.bars_off = off;  // full[kTapRing], empty[kTapRing] (uint64)
+  off += 4 * kTapRing;
   L.total = off * 4 + 1024;  // + alignment slack for the 1 KB-aligned base
   return L;
 }
 
-// Balanced decomposition: work units are (ear, group, tile, direction) with
-// group sizes nd in {q, q+1}; each persistent CTA takes a contiguous unit
-// range snapped to even directions (pairs are never split between CTAs), so
-// CTAs differ by at most one direction pair of one tile.
+// Balanced decomposition: work units are (ear, tile, direction); each
+// persistent CTA takes a contiguous unit range snapped to even directions
+// (pairs are never split between CTAs), so CTAs differ by at most one
+// direction pair of one tile.
 struct UnitMap {
-  int D, G, q, r, n_tiles;
+  int D, n_tiles;
   long long n_units;
-  __device__ void decode(long long u, int& e, int& g, int& j, int& dd, int& nd, int& dbeg) const {
+  __device__ void decode(long long u, int& e, int& j, int& dd) const {
     const long long per_ear = (long long)D * n_tiles;
     e = (int)(u / per_ear);
-    long long rem = u - (long long)e * per_ear;
-    const long long big = (long long)r * (q + 1) * n_tiles;  // units in the r groups of size q+1
-    long long loc;
-    if (rem < big) {
-      g = (int)(rem / ((long long)(q + 1) * n_tiles));
-      nd = q + 1;
-      loc = rem - (long long)g * (q + 1) * n_tiles;
-      dbeg = g * (q + 1);
-    } else {
-      const long long rr = rem - big;
-      const int gg = (int)(rr / ((long long)q * n_tiles));
-      g = r + gg;
-      nd = q;
-      loc = rr - (long long)gg * q * n_tiles;
-      dbeg = r * (q + 1) + gg * q;
-    }
-    j = (int)(loc / nd);
-    dd = (int)(loc - (long long)j * nd);
+    const long long rem = u - (long long)e * per_ear;
+    j = (int)(rem / D);
+    dd = (int)(rem - (long long)j * D);
   }
   __device__ long long snap(long long u) const {
     if (u >= n_units) return n_units;
-    int e, g, j, dd, nd, dbeg;
-    decode(u, e, g, j, dd, nd, dbeg);
+    int e, j, dd;
+    decode(u, e, j, dd);
     return u - (dd & 1);
   }
 };
@@ -123,16 +116,26 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
   // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
   float* smem = smem_raw + (((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) >> 2);
 
-  const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.dirs_per_group, a.tap_stride);
+  const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.tap_stride);
   float* s_x = smem + L.x_off;
   float* s_yf = smem + L.yf_off;
   float* s_halo = smem + L.halo_off;
   float* s_f = smem + L.f_off;
-  int4* s_taps = reinterpret_cast<int4*>(smem + L.taps_off);
-  int* s_nnz = reinterpret_cast<int*>(smem + L.nnz_off);
+  int4* s_ring = reinterpret_cast<int4*>(smem + L.ring_off);
+  int4* s_rnnz = reinterpret_cast<int4*>(smem + L.nnz_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars_off);
+  uint64_t* empty = full + kTapRing;
+  const int CP = L.chunk_pairs;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (warp == 0) tmem_alloc<C::COLS>(&s_tbase);
+  if (tid == 0) {
+    for (int i = 0; i < kTapRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kWarps);
+    }
+    mbar_fence_init();
+  }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -140,48 +143,48 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
 
   UnitMap um;
   um.D = a.dirs;
-  um.G = a.groups;
-  um.q = a.dirs / a.groups;
-  um.r = a.dirs % a.groups;
   um.n_tiles = a.n_tiles;
   um.n_units = (long long)a.ears * a.dirs * a.n_tiles;
   const long long u0 = um.snap(um.n_units * blockIdx.x / gridDim.x);
   const long long u1 = um.snap(um.n_units * (blockIdx.x + 1) / gridDim.x);
 
-  int cur_g = -1, cur_e = -1, prev_j = -2;
+  int cur_e = -1, prev_j = -2;
+  int chunk_base = 0;  // tap chunks consumed by this CTA so far (ring phase bookkeeping)
   float* st = smem + L.region_off + warp * kStageFloatsPerWarp;
   const int half = lane >> 4, inner = (lane & 15) * 16;
 
   for (long long u = u0; u < u1;) {
-    int e, g, j, dd0, nd, dbeg;
-    um.decode(u, e, g, j, dd0, nd, dbeg);
+    int e, j, dd0;
+    um.decode(u, e, j, dd0);
+    const int nd = a.dirs;
     const int dd1 = (int)min((long long)nd, dd0 + (u1 - u));
     u += dd1 - dd0;
     const long long T0 = (long long)j * kW;
-    const bool same_group = (g == cur_g && e == cur_e);
-    const bool reuse_halo = STAGE1 && same_group && (j == prev_j + 1);
+    const bool reuse_halo = STAGE1 && e == cur_e && (j == prev_j + 1);
+    const int p0 = dd0 >> 1, p1 = (dd1 + 1) >> 1;
+    const int nchunks = (p1 - p0 + CP - 1) / CP;
+    const int4* pairs_e = a.pairs + (long long)e * a.pairs_per_ear * a.tap_stride;
+    const int4* pnnz_e = a.pair_nnz + (long long)e * a.pairs_per_ear;
+    // tap-chunk producer (warp 0, elected lane): chunk c covers pairs p0 + c*CP ...
+    auto issue_chunk = [&](int c) {
+      const int g = chunk_base + c;
+      const int buf = g % kTapRing;
+      mbar_wait(&empty[buf], (unsigned)(((g / kTapRing) & 1) ^ 1));
+      const int pb = p0 + c * CP;
+      const int np = min(CP, p1 - pb);
+      const unsigned bytes_t = (unsigned)(np * a.tap_stride) * 16u;
+      mbar_arrive_expect_tx(&full[buf], bytes_t + (unsigned)np * 16u);
+      bulk_load(s_ring + buf * CP * a.tap_stride, pairs_e + (long long)pb * a.tap_stride, bytes_t, &full[buf]);
+      bulk_load(s_rnnz + buf * CP, pnnz_e + pb, (unsigned)np * 16u, &full[buf]);
+    };
 
     if (lane == 0) bulk_wait_read<0>();  // staging region is about to be reused
-    __syncthreads();  // previous item fully consumed (TMEM windows, smem region, s_taps)
-
-    // ---- tap table for (e, g), pair-interleaved ----------------------------
-    if (!same_group) {
-      const long long row0 = (long long)e * a.dirs + dbeg;
-      const int pairs = (nd + 1) / 2;
-      const int n = pairs * a.tap_stride;
-      const int2* src = a.taps + row0 * a.tap_stride;
-      for (int i = tid; i < n; i += kThreads) {
-        const int p = i / a.tap_stride, k = i - p * a.tap_stride;
-        const int2 A = src[(long long)(2 * p) * a.tap_stride + k];
-        const int2 B = (2 * p + 1 < nd) ? src[(long long)(2 * p + 1) * a.tap_stride + k] : make_int2(KWIN, 0);
-        s_taps[i] = make_int4(A.x, A.y, B.x, B.y);
-      }
-      for (int i = tid; i < 2 * pairs; i += kThreads) s_nnz[i] = (i < nd) ? a.row_nnz[row0 + i] : 0;
-      if (STAGE1 && e != cur_e)
-        for (int i = tid; i < a.lf_pad; i += kThreads) s_f[i] = a.f[(long long)e * a.lf_pad + i];
-      cur_g = g;
-      cur_e = e;
-    }
+    __syncthreads();  // previous item fully consumed (TMEM windows, smem region)
+    if (warp == 0 && elect_one())
+      for (int c = 0; c < min(kTapRing - 1, nchunks); ++c) issue_chunk(c);
+    if (STAGE1 && e != cur_e)
+      for (int i = tid; i < a.lf_pad; i += kThreads) s_f[i] = a.f[(long long)e * a.lf_pad + i];
+    cur_e = e;
     prev_j = j;
 
     // ---- y*f tile [T0 - YH, T0 + kW) -------------------------------------
@@ -250,10 +253,16 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
 
     // ---- sparse reflection stage, two directions per pass ------------------
     const long long col = T0 + (long long)warp * 32 * kR;
-    if (col >= a.out_len) continue;  // warp wholly past the row end: nothing to store
-    const int p0 = dd0 >> 1, p1 = (dd1 + 1) >> 1;
+    const bool store = col < a.out_len;  // warps wholly past the row end compute but store nothing
     for (int p = p0; p < p1; ++p) {
-      const int4* tp = s_taps + p * a.tap_stride;
+      const int c = (p - p0) / CP, kin = (p - p0) - c * CP;
+      const int g = chunk_base + c, buf = g % kTapRing;
+      if (kin == 0) {
+        if (warp == 0 && c + kTapRing - 1 < nchunks && elect_one()) issue_chunk(c + kTapRing - 1);
+        __syncwarp();
+        mbar_wait(&full[buf], (unsigned)((g / kTapRing) & 1));
+      }
+      const int4* tp = s_ring + (buf * CP + kin) * a.tap_stride;
       float accA[16], accB[16];
       if constexpr (NNZT > 0) {
         // software pipeline: the TMEM loads of tap k+1 are in flight while
@@ -294,7 +303,8 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
           tn = tnn;
         }
       } else {
-        const int nk = max(s_nnz[2 * p], s_nnz[2 * p + 1]);
+        const int4 pn = s_rnnz[buf * CP + kin];
+        const int nk = max(pn.x, pn.y);
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           accA[r] = 0.f;
@@ -314,6 +324,11 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
           }
         }
       }
+      if (kin == CP - 1 || p + 1 == p1) {  // this warp is done with the chunk's taps
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);
+      }
+      if (!store) continue;
       // ---- epilogue: stage 2 pairs (4 rows), then one proxy fence and
       //      TMA tensor stores of [2 rows x 256] boxes (clipped at out_len)
       const int pp = (p - p0) & 1;
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
         if (elect_one()) {
           for (int q = 0; q <= pp; ++q) {
             const int pq = p - pp + q;
-            const int rowA = e * a.dirs + dbeg + 2 * pq;
+            const int rowA = e * a.dirs + 2 * pq;
             const CUtensorMap* tm = (2 * pq + 1 < nd) ? &tm2 : &tm1;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -346,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
         }
       }
     }
+    chunk_base += nchunks;
   }
   if (lane == 0) bulk_wait_all();
   tmem_fence_before();
@@ -353,11 +369,38 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
   if (warp == 0) tmem_dealloc<C::COLS>(s_tbase);
 }
 
+// Interleave direction pairs of each segment of `seg` consecutive rows:
+// out[s][p][k] = {colA, vA, colB, vB} of rows (2p, 2p+1) of segment s (B padded
+// with a zero tap when the segment is odd); out_nnz[s][p] = {nnzA, nnzB, 0, 0}.
+__global__ void k_pair_taps(const int2* __restrict__ rows, const int* __restrict__ nnz, int n_seg, int seg,
+                            int stride, int kwin, int4* __restrict__ out, int4* __restrict__ out_nnz) {
+  const int P = (seg + 1) / 2;
+  const long long total = (long long)n_seg * P * stride;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % stride);
+    const long long sp = i / stride;
+    const int p = (int)(sp % P), s = (int)(sp / P);
+    const long long ra = (long long)s * seg + 2 * p, rb = ra + 1;
+    const int2 A = rows[ra * stride + k];
+    const int2 B = (2 * p + 1 < seg) ? rows[rb * stride + k] : make_int2(kwin, 0);
+    out[i] = make_int4(A.x, A.y, B.x, B.y);
+    if (k == 0) out_nnz[sp] = make_int4(nnz[ra], (2 * p + 1 < seg) ? nnz[rb] : 0, 0, 0);
+  }
+}
+
+cudaError_t launch_pair_taps(const int2* rows, const int* nnz, int n_seg, int seg, int stride, int kwin, int4* out,
+                             int4* out_nnz, cudaStream_t st) {
+  const long long total = (long long)n_seg * ((seg + 1) / 2) * stride;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+  k_pair_taps<<<std::max(blocks, 1), 256, 0, st>>>(rows, nnz, n_seg, seg, stride, kwin, out, out_nnz);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launch ----
 template <int KWIN, bool STAGE1, int NNZT>
 static cudaError_t launch_render_t(const RenderArgs& a, const RenderMaps& m, int sm_count, cudaStream_t st) {
   using C = RenderCfg<KWIN>;
-  const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.dirs_per_group, a.tap_stride);
+  const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.tap_stride);
   auto kern = k_render<KWIN, STAGE1, NNZT>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
@@ -429,8 +472,8 @@ int render_kwin_for(int K) {
   return -1;
 }
 
-size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int dpg, int tap_stride) {
-  return (size_t)render_smem_layout(kwin, stage1, lf_pad, dpg, tap_stride).total;
+size_t render_smem_bytes(int kwin, bool stage1, int lf_pad, int tap_stride) {
+  return (size_t)render_smem_layout(kwin, stage1, lf_pad, tap_stride).total;
 }
 
 cudaError_t launch_render(const RenderArgs& a, const RenderMaps& m, int kwin, bool stage1, int sm_count,

@@ -254,9 +254,14 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
     // ---- sparse reflection stage, two directions per pass ------------------
     const long long col = T0 + (long long)warp * 32 * kR;
     const bool store = col < a.out_len;  // warps wholly past the row end compute but store nothing
+    int c = 0, kin = 0, g = chunk_base, buf = chunk_base % kTapRing;  // chunk cursor (no division in the loop)
     for (int p = p0; p < p1; ++p) {
-      const int c = (p - p0) / CP, kin = (p - p0) - c * CP;
-      const int g = chunk_base + c, buf = g % kTapRing;
+      if (kin == CP) {
+        kin = 0;
+        ++c;
+        ++g;
+        buf = (buf + 1 == kTapRing) ? 0 : buf + 1;
+      }
       if (kin == 0) {
         if (warp == 0 && c + kTapRing - 1 < nchunks && elect_one()) issue_chunk(c + kTapRing - 1);
         __syncwarp();
@@ -328,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[buf]);
       }
+      ++kin;
       if (!store) continue;
       // ---- epilogue: stage 2 pairs (4 rows), then one proxy fence and
       //      TMA tensor stores of [2 rows x 256] boxes (clipped at out_len)

@@ -114,9 +114,11 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
 int toep_streamer_destroy(toep_streamer* s);
 /* Zero all carried history (stream-ordered). */
 int toep_streamer_reset(toep_streamer* s, void* stream);
-/* block: [S][block] new samples; out: [ears][block] = samples
- * [n*block, (n+1)*block) of the full mixdown after the n-th call. */
-int toep_streamer_step(toep_streamer* s, const float* block, float* out, void* stream);
+/* block: S rows of `block` new samples, source s at block + s*block_pitch
+ * (block_pitch >= block; e.g. a window into a resident [S][T] array);
+ * out: [ears][block] = samples [n*block, (n+1)*block) of the full mixdown
+ * after the n-th call. */
+int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, void* stream);
 
 #ifdef __cplusplus
 }

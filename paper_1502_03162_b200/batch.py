@@ -195,9 +195,10 @@ class StreamRenderer(_ModelSet):
 
     def step(self, block, out=None, stream=None):
         t = _lib.require_cuda()
-        if block.shape != (self.S, self.B) or block.dtype != t.float32 or not block.is_cuda:
+        if tuple(block.shape) != (self.S, self.B) or block.dtype != t.float32 or not block.is_cuda:
             raise DataError("block must be a float32 CUDA tensor of shape [S, B]")
-        block = block.contiguous()
+        if block.stride(1) != 1:
+            block = block.contiguous()  # rows may be a strided window of a resident [S, T] array
         if out is None:
             out = t.empty((self.ears, self.B), device="cuda", dtype=t.float32)
         self.streamer.step(block, out, stream)

@@ -730,11 +730,13 @@ int toep_streamer_reset(toep_streamer* s, void* stream) {
   return TOEP_OK;
 }
 
-int toep_streamer_step(toep_streamer* s, const float* block, float* out, void* stream) {
+int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, void* stream) {
   if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
   if (!block || !out) return fail(TOEP_ERR_INVALID, "null buffer");
+  if (s->S > 1 && block_pitch < s->B) return fail(TOEP_ERR_INVALID, "block pitch too small");
   StreamArgs a{};
   a.block = block;
+  a.block_pitch = s->S > 1 ? block_pitch : s->B;
   a.B = s->B;
   a.yhist = s->d_yhist;
   a.H = s->H;

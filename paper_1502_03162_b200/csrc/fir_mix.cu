@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
   for (int s = s0; s < s1; ++s) {
     __syncthreads();
     for (int i = tid; i < a.H; i += blockDim.x) s_w[i] = a.yhist[(long long)s * a.H + i];
-    for (int i = tid; i < a.B; i += blockDim.x) s_w[a.H + i] = a.block[(long long)s * a.B + i];
+    for (int i = tid; i < a.B; i += blockDim.x) s_w[a.H + i] = a.block[(long long)s * a.block_pitch + i];
     __syncthreads();
     const int dir = a.src_dir[s];
     for (int e = 0; e < a.ears; ++e) {

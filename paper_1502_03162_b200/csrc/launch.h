@@ -119,7 +119,8 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
 
 // Streaming block step (g-first, carried history).
 struct StreamArgs {
-  const float* block;    // [S][B] new samples
+  const float* block;    // new samples, source s at block + s * block_pitch
+  long long block_pitch;
   int B;
   float* yhist;          // [S][H] last H samples of every source (H >= K-1, multiple of 4)
   int H;

@@ -116,9 +116,10 @@ int toep_streamer_destroy(toep_streamer* s);
 int toep_streamer_reset(toep_streamer* s, void* stream);
 /* block: S rows of `block` new samples, source s at block + s*block_pitch
  * (block_pitch >= block; e.g. a window into a resident [S][T] array);
- * out: [ears][block] = samples [n*block, (n+1)*block) of the full mixdown
- * after the n-th call. */
-int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, void* stream);
+ * out: ear e at out + e*out_pitch, `block` samples = samples
+ * [n*block, (n+1)*block) of the full mixdown after the n-th call. */
+int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, int64_t out_pitch,
+                       void* stream);
 
 #ifdef __cplusplus
 }

@@ -84,7 +84,7 @@ def load_library(path: str = LIB_PATH):
         "toep_streamer_create": (ctypes.c_int, [_vp, _i32p, _i32, _i32, ctypes.POINTER(_vp)]),
         "toep_streamer_destroy": (ctypes.c_int, [_vp]),
         "toep_streamer_reset": (ctypes.c_int, [_vp, _vp]),
-        "toep_streamer_step": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+        "toep_streamer_step": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -274,7 +274,9 @@ class NativeStreamer:
 
     def step(self, block, out, stream=None):
         pitch = block.stride(0) if block.dim() == 2 else self.B
-        check(load_library().toep_streamer_step(self._h, dptr(block), int(pitch), dptr(out), stream_ptr(stream)))
+        opitch = out.stride(0) if out.dim() == 2 else self.B
+        check(load_library().toep_streamer_step(self._h, dptr(block), int(pitch), dptr(out), int(opitch),
+                                                stream_ptr(stream)))
 
     def __del__(self):
         h = getattr(self, "_h", None)

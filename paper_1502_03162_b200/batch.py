@@ -201,5 +201,7 @@ class StreamRenderer(_ModelSet):
             block = block.contiguous()  # rows may be a strided window of a resident [S, T] array
         if out is None:
             out = t.empty((self.ears, self.B), device="cuda", dtype=t.float32)
+        if tuple(out.shape) != (self.ears, self.B) or out.dtype != t.float32 or not out.is_cuda or out.stride(1) != 1:
+            raise DataError("out must be a float32 CUDA tensor [ears, B] with unit column stride")
         self.streamer.step(block, out, stream)
         return out

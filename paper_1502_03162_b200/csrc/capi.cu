@@ -730,10 +730,12 @@ int toep_streamer_reset(toep_streamer* s, void* stream) {
   return TOEP_OK;
 }
 
-int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, void* stream) {
+int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, int64_t out_pitch,
+                       void* stream) {
   if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
   if (!block || !out) return fail(TOEP_ERR_INVALID, "null buffer");
   if (s->S > 1 && block_pitch < s->B) return fail(TOEP_ERR_INVALID, "block pitch too small");
+  if (s->r->ears > 1 && out_pitch < s->B) return fail(TOEP_ERR_INVALID, "output pitch too small");
   StreamArgs a{};
   a.block = block;
   a.block_pitch = s->S > 1 ? block_pitch : s->B;
@@ -754,6 +756,7 @@ int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch
   a.f = s->r->d_f;
   a.lf_pad = s->r->lf_pad;
   a.out = out;
+  a.out_pitch = s->r->ears > 1 ? out_pitch : s->B;
   a.ctas = s->ctas;
   a.ticket = s->d_ticket;
   cudaError_t e = launch_stream_step(a, S(stream));

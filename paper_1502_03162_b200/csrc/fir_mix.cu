@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     for (int t = tid; t < a.B; t += blockDim.x) {
       float o = 0.f;
       for (int jj = 0; jj < a.lf_pad; ++jj) o = fmaf(s_f[jj], s_z[a.zh + t - jj], o);
-      a.out[(long long)e * a.B + t] = o;
+      a.out[(long long)e * a.out_pitch + t] = o;
     }
     __syncthreads();
     for (int i = tid; i < a.zh; i += blockDim.x) a.zhist[(long long)e * a.zh + i] = s_z[a.B + i];

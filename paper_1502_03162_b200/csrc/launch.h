@@ -137,7 +137,8 @@ struct StreamArgs {
   int zh;                // history length of z (multiple of 16, >= Lf-1)
   const float* f;        // [ears][lf_pad]
   int lf_pad;
-  float* out;            // [ears][B]
+  float* out;            // ear e at out + e * out_pitch, B samples
+  long long out_pitch;
   int ctas;
   unsigned int* ticket;  // zero-initialised device counter owned by the stream state
 };

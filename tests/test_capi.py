@@ -78,5 +78,5 @@ def test_null_handles_rejected():
     assert L.toep_renderer_destroy(None) == 0
     assert L.toep_renderer_render(None, None, 0, None, 0, None) == _lib.TOEP_ERR_INVALID
     assert L.toep_mixer_partial(None, None, 0, 0, 0, None, 0, None) == _lib.TOEP_ERR_INVALID
-    assert L.toep_streamer_step(None, None, 0, None, None) == _lib.TOEP_ERR_INVALID
+    assert L.toep_streamer_step(None, None, 0, None, 0, None) == _lib.TOEP_ERR_INVALID
     assert L.toep_renderer_out_len(None, 10) == -1

@@ -216,6 +216,12 @@ def test_streaming_equals_offline(mods, cuda):
     z = torch.zeros((cfg.sources, 256), device="cuda")
     tail = st.step(z).clone()
     assert rel_l2(tail[:, :199].cpu().numpy(), offline[:, cfg.ny:].cpu().numpy()) < TOL
+    # strided windows of resident arrays in and out (as the cfg4 tool streams)
+    st.reset()
+    full = torch.empty((2, cfg.ny), device="cuda")
+    for b in range(cfg.ny // 256):
+        st.step(y[:, b * 256:(b + 1) * 256], out=full[:, b * 256:(b + 1) * 256])
+    assert rel_l2(full.cpu().numpy(), offline[:, :cfg.ny].cpu().numpy()) < TOL
     # reset restarts from silence
     st.reset()
     again = st.step(y[:, :256].contiguous())

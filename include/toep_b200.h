@@ -109,13 +109,15 @@ int toep_mixer_finish(const toep_mixer* m, const float* z, int64_t z_pitch, floa
 
 /* ---- streaming: fixed block size, carried overlap history ---------------- */
 typedef struct toep_streamer toep_streamer;
+/* block: multiple of 4 in [4, 256]; ears <= 2. */
 int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, int32_t n_src, int32_t block,
                          toep_streamer** out);
 int toep_streamer_destroy(toep_streamer* s);
 /* Zero all carried history (stream-ordered). */
 int toep_streamer_reset(toep_streamer* s, void* stream);
 /* block: S rows of `block` new samples, source s at block + s*block_pitch
- * (block_pitch >= block; e.g. a window into a resident [S][T] array);
+ * (block_pitch >= block, multiple of 4, block 16-byte aligned; e.g. a window
+ * into a resident [S][T] array);
  * out: ear e at out + e*out_pitch, `block` samples = samples
  * [n*block, (n+1)*block) of the full mixdown after the n-th call. */
 int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch, float* out, int64_t out_pitch,

@@ -205,3 +205,22 @@ class StreamRenderer(_ModelSet):
             raise DataError("out must be a float32 CUDA tensor [ears, B] with unit column stride")
         self.streamer.step(block, out, stream)
         return out
+
+    def capture(self, y, out, blocks: int | None = None):
+        """CUDA graph of consecutive steps over a device-resident [S, T] input.
+
+        Block b reads y[:, b*B:(b+1)*B] and writes out[:, b*B:(b+1)*B]; replaying
+        the graph streams the whole signal with one host launch (the
+        per-block host launch overhead disappears; each node is one kernel).
+        """
+        t = _lib.require_cuda()
+        n = (y.shape[1] // self.B) if blocks is None else int(blocks)
+        g = t.cuda.CUDAGraph()
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):
+            with t.cuda.graph(g, stream=s):
+                for b in range(n):
+                    self.step(y[:, b * self.B:(b + 1) * self.B], out=out[:, b * self.B:(b + 1) * self.B])
+        t.cuda.current_stream().wait_stream(s)
+        return g

@@ -667,6 +667,7 @@ struct toep_streamer {
   float* d_yhist = nullptr;
   float* d_zhist = nullptr;
   float* d_part = nullptr;
+  float* d_gpart = nullptr;
   unsigned int* d_ticket = nullptr;
 };
 
@@ -678,7 +679,8 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
   *out = nullptr;
   if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
   if (n_src < 1 || !src_dir_host) return fail(TOEP_ERR_INVALID, "need at least one source");
-  if (block < 1 || block > 1024) return fail(TOEP_ERR_UNSUPPORTED, "block size must be in [1, 1024]");
+  if (block < 4 || block > 256 || block % 4) return fail(TOEP_ERR_UNSUPPORTED, "block size must be a multiple of 4 in [4, 256]");
+  if (r->ears > 2) return fail(TOEP_ERR_UNSUPPORTED, "streaming supports at most 2 ears");
   if (r->g->length > 4096) return fail(TOEP_ERR_UNSUPPORTED, "streaming supports reflection length <= 4096");
   for (int s = 0; s < n_src; ++s)
     if (src_dir_host[s] < 0 || src_dir_host[s] >= r->dirs)
@@ -690,17 +692,20 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
   s->B = block;
   s->H = (int)round_up(std::max(1, r->g->length - 1), 4);
   s->zh = r->lf_pad;
-  s->spc = 8;
+  // 4 sources per CTA: ~1 CTA per SM for 512 sources, short per-thread tap chains
+  s->spc = std::max(1, std::min(4, (96 * 1024 / 4) / (s->H + block + 2 * r->ears * r->g->tap_stride + r->ears)));
   s->ctas = (n_src + s->spc - 1) / s->spc;
+  const int groups = (s->ctas + 15) / 16;
   cudaError_t e = cudaMalloc(&s->d_dir, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(s->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&s->d_yhist, (size_t)n_src * s->H * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_zhist, (size_t)r->ears * s->zh * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_part, (size_t)s->ctas * r->ears * block * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&s->d_ticket, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_gpart, (size_t)groups * r->ears * block * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_ticket, (groups + 1) * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(s->d_yhist, 0, (size_t)n_src * s->H * sizeof(float));
   if (e == cudaSuccess) e = cudaMemset(s->d_zhist, 0, (size_t)r->ears * s->zh * sizeof(float));
-  if (e == cudaSuccess) e = cudaMemset(s->d_ticket, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(s->d_ticket, 0, (groups + 1) * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     toep_streamer_destroy(s);
@@ -716,6 +721,7 @@ int toep_streamer_destroy(toep_streamer* s) {
   if (s->d_yhist) cudaFree(s->d_yhist);
   if (s->d_zhist) cudaFree(s->d_zhist);
   if (s->d_part) cudaFree(s->d_part);
+  if (s->d_gpart) cudaFree(s->d_gpart);
   if (s->d_ticket) cudaFree(s->d_ticket);
   delete s;
   return TOEP_OK;
@@ -726,7 +732,7 @@ int toep_streamer_reset(toep_streamer* s, void* stream) {
   cudaStream_t st = S(stream);
   TOEP_CUDA(cudaMemsetAsync(s->d_yhist, 0, (size_t)s->S * s->H * sizeof(float), st));
   TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)s->r->ears * s->zh * sizeof(float), st));
-  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, sizeof(unsigned int), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, ((s->ctas + 15) / 16 + 1) * sizeof(unsigned int), st));
   return TOEP_OK;
 }
 
@@ -735,6 +741,8 @@ int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch
   if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
   if (!block || !out) return fail(TOEP_ERR_INVALID, "null buffer");
   if (s->S > 1 && block_pitch < s->B) return fail(TOEP_ERR_INVALID, "block pitch too small");
+  if ((reinterpret_cast<uintptr_t>(block) & 15) || (s->S > 1 && block_pitch % 4))
+    return fail(TOEP_ERR_INVALID, "block must be 16-byte aligned with a pitch multiple of 4");
   if (s->r->ears > 1 && out_pitch < s->B) return fail(TOEP_ERR_INVALID, "output pitch too small");
   StreamArgs a{};
   a.block = block;
@@ -751,6 +759,7 @@ int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch
   a.ears = s->r->ears;
   a.src_per_cta = s->spc;
   a.part = s->d_part;
+  a.gpart = s->d_gpart;
   a.zhist = s->d_zhist;
   a.zh = s->zh;
   a.f = s->r->d_f;

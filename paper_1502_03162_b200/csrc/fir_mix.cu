@@ -502,82 +502,137 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
 }
 
 // ------------------------------------------------------ streaming block ----
-// One launch per block of B samples: every CTA owns src_per_cta sources,
-// forms [history | block] windows in shared memory, accumulates both ears'
-// partial z over its sources, and rolls the source history forward.  The
-// last CTA to finish (atomic ticket) sums the partials in fixed CTA order,
+// One launch per block of B <= 256 samples (latency path).  CTA c owns
+// src_per_cta sources; thread t owns output sample t for both ears.  The CTA
+// loads its sources' [history | block] windows and tap rows into shared
+// memory in one vectorised round, accumulates per-thread (3 instructions per
+// tap: broadcast tap, window sample, FFMA), writes one partial and rolls the
+// sources' history.  Partials are reduced deterministically in two ticketed
+// levels (groups of kStreamGroup CTAs, then the groups), and the very last CTA
 // applies f_e over [z history | z block] and rolls the z history.
+constexpr int kStreamGroup = 16;
+
+__device__ __forceinline__ bool stream_last_arrival(unsigned int* ticket, unsigned int n) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == n - 1);
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
 __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
-  unsigned int* ticket = a.ticket;
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x;
-  float* s_w = sm;  // [L] window of current source
-  __shared__ bool s_last;
+  const int L = a.H + a.B;  // multiple of 4 (host checks)
   const int s0 = blockIdx.x * a.src_per_cta;
-  const int s1 = min(a.S, s0 + a.src_per_cta);
-  for (int e = 0; e < a.ears; ++e)
-    for (int t = tid; t < a.B; t += blockDim.x) a.part[((long long)blockIdx.x * a.ears + e) * a.B + t] = 0.f;
-  float acc[2][4];
-  for (int s = s0; s < s1; ++s) {
-    __syncthreads();
-    for (int i = tid; i < a.H; i += blockDim.x) s_w[i] = a.yhist[(long long)s * a.H + i];
-    for (int i = tid; i < a.B; i += blockDim.x) s_w[a.H + i] = a.block[(long long)s * a.block_pitch + i];
-    __syncthreads();
-    const int dir = a.src_dir[s];
-    for (int e = 0; e < a.ears; ++e) {
-      const long long row = (long long)e * a.dirs + dir;
-      const int2* tp = a.taps + row * a.tap_stride;
-      const int nnz = a.row_nnz[row];
-      for (int q = 0; q < 4; ++q) acc[e][q] = 0.f;
-      for (int k = 0; k < nnz; ++k) {
-        const int2 tv = tp[k];
-        const float v = __int_as_float(tv.y);
-        for (int q = 0; q < 4; ++q) {
-          const int t = tid + 256 * q;
-          if (t < a.B) acc[e][q] = fmaf(v, s_w[a.H + t - tv.x], acc[e][q]);
-        }
-      }
-      for (int q = 0; q < 4; ++q) {
-        const int t = tid + 256 * q;
-        if (t < a.B) a.part[((long long)blockIdx.x * a.ears + e) * a.B + t] += acc[e][q];
-      }
+  const int ns = min(a.S - s0, a.src_per_cta);
+  float* s_w = sm;                                                // [ns][L]
+  int2* s_tap = reinterpret_cast<int2*>(sm + a.src_per_cta * L);  // [ns][ears][tap_stride]
+  int* s_nnz = reinterpret_cast<int*>(s_tap + a.src_per_cta * a.ears * a.tap_stride);
+  {
+    const int q4 = L / 4, h4 = a.H / 4;
+    for (int i = tid; i < ns * q4; i += blockDim.x) {
+      const int s = i / q4, q = i - s * q4;
+      float4 v;
+      if (q < h4) v = *reinterpret_cast<const float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q);
+      else v = __ldg(reinterpret_cast<const float4*>(a.block + (long long)(s0 + s) * a.block_pitch) + (q - h4));
+      *reinterpret_cast<float4*>(&s_w[s * L + 4 * q]) = v;
     }
-    __syncthreads();
-    // roll this source's history: keep the last H samples of [hist | block]
-    for (int i = tid; i < a.H; i += blockDim.x) a.yhist[(long long)s * a.H + i] = s_w[a.B + i];
+    for (int i = tid; i < ns * a.ears * a.tap_stride; i += blockDim.x) {
+      const int se = i / a.tap_stride, k = i - se * a.tap_stride;
+      const int s = se / a.ears, e = se - s * a.ears;
+      const long long row = (long long)e * a.dirs + a.src_dir[s0 + s];
+      s_tap[i] = a.taps[row * a.tap_stride + k];
+      if (k == 0) s_nnz[se] = a.row_nnz[row];
+    }
   }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // z window per ear: [zhist (zh) | zblock (B)], out = f * z over the block
-  float* s_z = sm;
-  float* s_f = sm + (a.zh + a.B);
-  for (int e = 0; e < a.ears; ++e) {
-    __syncthreads();
-    for (int i = tid; i < a.zh; i += blockDim.x) s_z[i] = a.zhist[(long long)e * a.zh + i];
-    for (int t = tid; t < a.B; t += blockDim.x) {
-      float zz = 0.f;
-      for (int c = 0; c < gridDim.x; ++c) zz += a.part[((long long)c * a.ears + e) * a.B + t];
-      s_z[a.zh + t] = zz;
+  const int t = tid;
+  float acc0 = 0.f, acc1 = 0.f;
+  if (t < a.B) {
+    for (int s = 0; s < ns; ++s) {
+      const float* w = s_w + s * L + a.H + t;
+      const int2* t0 = s_tap + (s * a.ears) * a.tap_stride;
+      const int n0 = s_nnz[s * a.ears];
+#pragma unroll 4
+      for (int k = 0; k < n0; ++k) acc0 = fmaf(__int_as_float(t0[k].y), w[-t0[k].x], acc0);
+      if (a.ears > 1) {
+        const int2* t1 = t0 + a.tap_stride;
+        const int n1 = s_nnz[s * a.ears + 1];
+#pragma unroll 4
+        for (int k = 0; k < n1; ++k) acc1 = fmaf(__int_as_float(t1[k].y), w[-t1[k].x], acc1);
+      }
     }
-    for (int i = tid; i < a.lf_pad; i += blockDim.x) s_f[i] = a.f[(long long)e * a.lf_pad + i];
-    __syncthreads();
-    for (int t = tid; t < a.B; t += blockDim.x) {
-      float o = 0.f;
-      for (int jj = 0; jj < a.lf_pad; ++jj) o = fmaf(s_f[jj], s_z[a.zh + t - jj], o);
-      a.out[(long long)e * a.out_pitch + t] = o;
-    }
-    __syncthreads();
-    for (int i = tid; i < a.zh; i += blockDim.x) a.zhist[(long long)e * a.zh + i] = s_z[a.B + i];
+    a.part[((long long)blockIdx.x * a.ears) * a.B + t] = acc0;
+    if (a.ears > 1) a.part[((long long)blockIdx.x * a.ears + 1) * a.B + t] = acc1;
   }
-  if (tid == 0) *ticket = 0u;
+  // roll the sources' history: keep the last H samples of [hist | block]
+  for (int i = tid; i < ns * (a.H / 4); i += blockDim.x) {
+    const int s = i / (a.H / 4), q = i - s * (a.H / 4);
+    *reinterpret_cast<float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q) =
+        *reinterpret_cast<const float4*>(&s_w[s * L + a.B + 4 * q]);
+  }
+  // ---- level 1: the last CTA of each group sums the group's partials --------
+  const int groups = (gridDim.x + kStreamGroup - 1) / kStreamGroup;
+  const int grp = blockIdx.x / kStreamGroup;
+  const int c0 = grp * kStreamGroup, nc = min((int)gridDim.x - c0, kStreamGroup);
+  if (!stream_last_arrival(a.ticket + grp, nc)) return;
+  const long long cs = (long long)a.ears * a.B;
+  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
+    float z[kStreamGroup];
+#pragma unroll
+    for (int u = 0; u < kStreamGroup; ++u) z[u] = u < nc ? __ldcg(a.part + (c0 + u) * cs + i) : 0.f;
+#pragma unroll
+    for (int w = kStreamGroup / 2; w > 0; w /= 2)
+#pragma unroll
+      for (int u = 0; u < w; ++u) z[u] += z[u + w];
+    a.gpart[grp * cs + i] = z[0];
+  }
+  if (tid == 0) a.ticket[grp] = 0u;
+  // ---- level 2: the last group finishes: z = sum of groups, out = f * z -----
+  if (!stream_last_arrival(a.ticket + groups, groups)) return;
+  float* s_z = sm;                          // [ears][zh + B]
+  float* s_f = sm + a.ears * (a.zh + a.B);  // [ears][lf_pad]
+  for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
+    const int e = i / a.zh, k = i - e * a.zh;
+    s_z[e * (a.zh + a.B) + k] = a.zhist[(long long)e * a.zh + k];
+  }
+  for (int i = tid; i < a.ears * a.lf_pad; i += blockDim.x) s_f[i] = a.f[i];
+  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
+    const int e = i / a.B, tt = i - e * a.B;
+    float z = 0.f;
+    for (int g = 0; g < groups; ++g) z += __ldcg(a.gpart + g * cs + i);
+    s_z[e * (a.zh + a.B) + a.zh + tt] = z;
+  }
+  __syncthreads();
+  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
+    const int e = i / a.B, tt = i - e * a.B;
+    const float* z = s_z + e * (a.zh + a.B) + a.zh + tt;
+    const float* ff = s_f + e * a.lf_pad;
+    float o = 0.f;
+#pragma unroll 8
+    for (int jj = 0; jj < a.lf_pad; ++jj) o = fmaf(ff[jj], z[-jj], o);
+    a.out[(long long)e * a.out_pitch + tt] = o;
+  }
+  __syncthreads();
+  for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
+    const int e = i / a.zh, k = i - e * a.zh;
+    a.zhist[(long long)e * a.zh + k] = s_z[e * (a.zh + a.B) + a.B + k];
+  }
+  if (tid == 0) a.ticket[groups] = 0u;
 }
 
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)max(a.H + a.B, a.zh + a.B + a.lf_pad) * 4;
+  const size_t per_cta = (size_t)a.src_per_cta * (a.H + a.B) + (size_t)a.src_per_cta * a.ears * a.tap_stride * 2 +
+                         (size_t)a.src_per_cta * a.ears;
+  const size_t fin = (size_t)a.ears * (a.zh + a.B + a.lf_pad);
+  const size_t smem = std::max(per_cta, fin) * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_stream_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   k_stream_step<<<a.ctas, 256, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -133,6 +133,7 @@ struct StreamArgs {
   int ears;
   int src_per_cta;
   float* part;           // [ctas][ears][B]
+  float* gpart;          // [ceil(ctas/16)][ears][B] level-1 sums
   float* zhist;          // [ears][lf_pad] last lf_pad-? samples of z (H2 >= Lf-1)
   int zh;                // history length of z (multiple of 16, >= Lf-1)
   const float* f;        // [ears][lf_pad]
@@ -140,7 +141,7 @@ struct StreamArgs {
   float* out;            // ear e at out + e * out_pitch, B samples
   long long out_pitch;
   int ctas;
-  unsigned int* ticket;  // zero-initialised device counter owned by the stream state
+  unsigned int* ticket;  // [ceil(ctas/16) + 1] zero-initialised counters owned by the stream state
 };
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st);
 

@@ -147,6 +147,22 @@ __host__ __device__ constexpr int padded_len(int n) { return n + ((n + 31) / 32)
 // `x` is the padded tile, `base` a logical index (multiple of 16) with at
 // least ntaps_padded earlier samples available; `h` is zero-padded to a
 // multiple of 16 in shared memory.  256 FFMA per 8+4 LDS.128.
+// Packed fp32 pair arithmetic (sm_100 FFMA2 / FMUL2): {a0,a1} = {x0,x1} * v (+ {a0,a1}).
+// Two correctly rounded fp32 FMAs per instruction -- bitwise the same as two fmaf,
+// half the issue slots.  The ptxas form takes v as a broadcast scalar register.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float v) {
+  asm("{\n\t.reg .b64 a, x, v;\n\tmov.b64 a, {%0,%1};\n\tmov.b64 x, {%2,%3};\n\tmov.b64 v, {%4,%4};\n\t"
+      "fma.rn.f32x2 a, x, v, a;\n\tmov.b64 {%0,%1}, a;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(x0), "f"(x1), "f"(v));
+}
+__device__ __forceinline__ void fmul2(float& a0, float& a1, float x0, float x1, float v) {
+  asm("{\n\t.reg .b64 a, x, v;\n\tmov.b64 x, {%2,%3};\n\tmov.b64 v, {%4,%4};\n\t"
+      "mul.rn.f32x2 a, x, v;\n\tmov.b64 {%0,%1}, a;\n}"
+      : "=f"(a0), "=f"(a1)
+      : "f"(x0), "f"(x1), "f"(v));
+}
+
 __device__ __forceinline__ void fir16_block(float (&acc)[16], const float* __restrict__ x, int base,
                                             const float* __restrict__ h, int ntaps_padded) {
   for (int j0 = 0; j0 < ntaps_padded; j0 += 16) {

@@ -293,15 +293,15 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
           const float va = __int_as_float(t.y), vb = __int_as_float(t.w);
           if (k == 0) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-              accA[r] = va * XA[r];
-              accB[r] = vb * XB[r];
+            for (int r = 0; r < 16; r += 2) {
+              fmul2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+              fmul2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
             }
           } else {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-              accA[r] = fmaf(va, XA[r], accA[r]);
-              accB[r] = fmaf(vb, XB[r], accB[r]);
+            for (int r = 0; r < 16; r += 2) {
+              ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+              ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
             }
           }
           t = tn;
@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(kThreads, (512 / (kR + KWIN)) > 3 ? TOEP_RENDE
           tmem_wait_ld();
           const float va = __int_as_float(t.y), vb = __int_as_float(t.w);
 #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            accA[r] = fmaf(va, XA[r], accA[r]);
-            accB[r] = fmaf(vb, XB[r], accB[r]);
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
           }
         }
       }

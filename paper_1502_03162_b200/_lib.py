@@ -14,7 +14,7 @@ import numpy as np
 from .errors import DataError
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libtoep_b200.so")
+LIB_PATH = os.environ.get("TOEP_LIB") or os.path.join(PKG_DIR, "libtoep_b200.so")  # TOEP_LIB: experiment builds
 
 TOEP_OK, TOEP_ERR_INVALID, TOEP_ERR_CUDA, TOEP_ERR_NOMEM, TOEP_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 

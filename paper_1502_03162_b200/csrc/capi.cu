@@ -2,6 +2,7 @@
 // reference's DataError rules; kernels live in render.cu / fir_mix.cu.
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -323,6 +324,7 @@ struct toep_renderer {
   float* d_f = nullptr;      // [ears][lf_pad]
   int4* d_pairs = nullptr;   // [ears][pairs_per_ear][tap_stride] pair-interleaved taps (k_render)
   int4* d_pnnz = nullptr;    // [ears][pairs_per_ear]
+  int* d_nonfinite = nullptr;  // sticky flag: a kernel read a non-finite input sample
 };
 
 extern "C" {
@@ -349,6 +351,8 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
   for (int e = 0; e < ears; ++e)
     for (int j = 0; j < lf; ++j) fp[(size_t)e * r->lf_pad + j] = f_host[(size_t)e * lf + j];
   cudaError_t e = cudaMalloc(&r->d_f, fp.size() * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_nonfinite, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(r->d_nonfinite, 0, sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(r->d_f, fp.data(), fp.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (g->kwin > 0) {
     r->pairs_per_ear = (dirs + 1) / 2;
@@ -370,6 +374,7 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
 int toep_renderer_destroy(toep_renderer* r) {
   if (!r) return TOEP_OK;
   if (r->d_f) cudaFree(r->d_f);
+  if (r->d_nonfinite) cudaFree(r->d_nonfinite);
   if (r->d_pairs) cudaFree(r->d_pairs);
   if (r->d_pnnz) cudaFree(r->d_pnnz);
   delete r;
@@ -476,6 +481,7 @@ struct toep_mixer {
   bool use_buckets = false;
   int* d_bsrc = nullptr;        // sources sorted by direction
   int* d_bptr = nullptr;        // bucket b = d_bsrc[d_bptr[b] .. d_bptr[b+1])
+  int* d_bdir = nullptr;        // direction of bucket b
   int4* d_bsteps = nullptr;     // one step per bucket {b, dir, 1, 1}
   float* d_yb = nullptr;        // bucket sums [buckets][yb_pitch]
   size_t yb_bytes = 0;
@@ -485,6 +491,25 @@ struct toep_mixer {
 };
 
 static constexpr int kSrcPerGroup = 256;
+
+static bool mix_legacy() {
+  const char* ev = getenv("TOEP_MIX_LEGACY");
+  return ev && atoi(ev) != 0;
+}
+
+static cudaError_t ensure_part(toep_mixer* m, size_t need, cudaStream_t st) {
+  if (need <= m->part_bytes) return cudaSuccess;
+  if (m->d_part) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    cudaFree(m->d_part);
+    m->d_part = nullptr;
+    m->part_bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&m->d_part, need);
+  if (e == cudaSuccess) m->part_bytes = need;
+  return e;
+}
 
 extern "C" {
 
@@ -512,6 +537,7 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bsrc, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bptr, (n_src + 1) * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bsteps, n_src * sizeof(int4));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_bdir, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(m->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     toep_mixer_destroy(m);
@@ -528,6 +554,7 @@ int toep_mixer_destroy(toep_mixer* m) {
   if (m->d_bsrc) cudaFree(m->d_bsrc);
   if (m->d_bptr) cudaFree(m->d_bptr);
   if (m->d_bsteps) cudaFree(m->d_bsteps);
+  if (m->d_bdir) cudaFree(m->d_bdir);
   if (m->d_yb) cudaFree(m->d_yb);
   if (m->d_part) cudaFree(m->d_part);
   delete m;
@@ -558,6 +585,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     std::vector<int4> steps(count);
     std::vector<int> bptr(1, 0);
     std::vector<int4> bsteps;
+    std::vector<int> bdir;
     for (int p = 0; p < count; ++p) {
       const int d = dir[ord[p]];
       const bool first = (p % kSrcPerGroup == 0) || dir[ord[p - 1]] != d;
@@ -565,6 +593,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
       steps[p] = make_int4(ord[p], d, first ? 1 : 0, last ? 1 : 0);
       if (p + 1 == count || dir[ord[p + 1]] != d) {
         bsteps.push_back(make_int4((int)bsteps.size(), d, 1, 1));
+        bdir.push_back(d);
         bptr.push_back(p + 1);
       }
     }
@@ -574,11 +603,50 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     TOEP_CUDA(cudaMemcpyAsync(m->d_bsrc, ord.data(), count * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaMemcpyAsync(m->d_bptr, bptr.data(), bptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaMemcpyAsync(m->d_bsteps, bsteps.data(), bsteps.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    TOEP_CUDA(cudaMemcpyAsync(m->d_bdir, bdir.data(), bdir.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaStreamSynchronize(st));
     m->order_s0 = s0;
     m->order_count = count;
   }
-  // sources -> per-direction sums (one HBM streaming pass) when directions repeat
+  const int n_tiles = (int)((m->zlen + kW - 1) / kW);
+  const long long part_pitch = (long long)n_tiles * kW;
+  if (!mix_legacy()) {
+    // one pass: k_mixb sums each bucket's sources per tile on the fly
+    const int sm = sm_count_cached();
+    const long long slots = (long long)sm * (512 / (kR + g->kwin));
+    // >= ~24 items per persistent CTA keeps the tail short; fewer groups keep the partials small
+    long long bpg = ((long long)m->buckets * n_tiles + 24 * slots - 1) / (24 * slots);
+    bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, 512), m->buckets));  // <= kMixBMaxBuckets
+    const int groups = (int)((m->buckets + bpg - 1) / bpg);
+    TOEP_CUDA(ensure_part(m, (size_t)groups * m->r->ears * part_pitch * sizeof(float), st));
+    MixBArgs a{};
+    a.y = y;
+    a.T = m->T;
+    a.y_pitch = count > 1 ? y_pitch : round_up(m->T, 4);
+    a.bsrc = m->d_bsrc;
+    a.bptr = m->d_bptr;
+    a.bdir = m->d_bdir;
+    a.buckets = m->buckets;
+    a.buckets_per_group = (int)bpg;
+    a.groups = groups;
+    a.n_tiles = n_tiles;
+    a.n_items = (long long)groups * n_tiles;
+    a.taps = g->d_kw;
+    a.row_nnz = g->d_nnz;
+    a.tap_stride = g->tap_stride;
+    a.dirs = m->r->dirs;
+    a.ears = m->r->ears;
+    a.part = m->d_part;
+    a.part_pitch = part_pitch;
+    a.zlen = m->zlen;
+    a.nonfinite = m->r->d_nonfinite;
+    cudaError_t e = launch_mixb(a, g->kwin, g->uniform ? g->max_nnz : 0, sm, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_mixb");
+    e = launch_mix_reduce(m->d_part, groups, m->r->ears, part_pitch, m->zlen, z, z_pitch, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_mix_reduce");
+    return TOEP_OK;
+  }
+  // legacy two-pass path (TOEP_MIX_LEGACY=1): per-direction sums in HBM, then k_mix
   const float* xs = y;
   long long xs_pitch = y_pitch;
   int nsteps = count;
@@ -606,19 +674,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     steps_dev = m->d_bsteps;
   }
   const int groups = (nsteps + kSrcPerGroup - 1) / kSrcPerGroup;
-  const int n_tiles = (int)((m->zlen + kW - 1) / kW);
-  const long long part_pitch = (long long)n_tiles * kW;
-  const size_t need = (size_t)groups * m->r->ears * part_pitch * sizeof(float);
-  if (need > m->part_bytes) {
-    if (m->d_part) {
-      TOEP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(m->d_part);
-      m->d_part = nullptr;
-      m->part_bytes = 0;
-    }
-    TOEP_CUDA(cudaMalloc(&m->d_part, need));
-    m->part_bytes = need;
-  }
+  TOEP_CUDA(ensure_part(m, (size_t)groups * m->r->ears * part_pitch * sizeof(float), st));
   MixArgs a{};
   a.y = xs;
   a.steps = steps_dev;

@@ -156,6 +156,12 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, 
       : "+f"(a0), "+f"(a1)
       : "f"(x0), "f"(x1), "f"(v));
 }
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float x0, float x1) {
+  asm("{\n\t.reg .b64 a, x;\n\tmov.b64 a, {%0,%1};\n\tmov.b64 x, {%2,%3};\n\t"
+      "add.rn.f32x2 a, a, x;\n\tmov.b64 {%0,%1}, a;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(x0), "f"(x1));
+}
 __device__ __forceinline__ void fmul2(float& a0, float& a1, float x0, float x1, float v) {
   asm("{\n\t.reg .b64 a, x, v;\n\tmov.b64 x, {%2,%3};\n\tmov.b64 v, {%4,%4};\n\t"
       "mul.rn.f32x2 a, x, v;\n\tmov.b64 {%0,%1}, a;\n}"

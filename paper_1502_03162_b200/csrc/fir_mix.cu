@@ -147,15 +147,11 @@ __host__ __device__ inline MixLayout mix_layout(int KWIN, int tap_stride) {
   L.meta_off = L.taps_off + 4 * tap_stride;               // int4 {first, last, dir, src}
   L.stage_floats = (L.meta_off + 4 + 31) & ~31;
   L.accum_off = kMixStages * L.stage_floats;              // slice sums, then the item's store staging
-  L.warp_floats = L.accum_off + ((L.slice > 2 * 32 * kR ? L.slice : 2 * 32 * kR) + 31 & ~31);
+  const int acc_floats = padded_len(L.slice);             // bank-padded slice sum
+  L.warp_floats = L.accum_off + ((acc_floats > 2 * 32 * kR ? acc_floats : 2 * 32 * kR) + 31 & ~31);
   L.bars_off = kWarps * L.warp_floats;                    // [warps][kMixStages] uint64
   L.total = (L.bars_off + 2 * kWarps * kMixStages) * 4 + 128;
   return L;
-}
-
-__device__ __forceinline__ int mix_group_size(const MixArgs& a, long long item) {
-  const int grp = (int)(item / a.n_tiles);
-  return min(a.src_per_group, a.S - grp * a.src_per_group);
 }
 
 template <int KWIN, int NNZT>
@@ -184,49 +180,58 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
   const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
   const long long it0 = (long long)blockIdx.x * per;
   const long long it1 = min(a.n_items, it0 + per);
+  if (it0 >= it1) {
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<COLS>(s_tbase);
+    return;
+  }
+  constexpr int SLICE = 32 * kR + KWIN;          // == L.slice
   const int slice_sig0 = 32 * kR * warp - KWIN;  // signal offset of the slice relative to T0
 
-  // ---- producer cursor (lane 0 issues; the warp shares step-table chunks) ----
-  long long p_item = it0;
+  // ---- producer cursor: (group, tile, position) advanced incrementally; the
+  //      group's step entries are read 32 at a time (one coalesced load per
+  //      warp, prefetched a chunk ahead) and broadcast by shuffle.
+  int p_grp = (int)(it0 / a.n_tiles), p_j = (int)(it0 - (long long)p_grp * a.n_tiles);
+  int p_ns = min(a.src_per_group, a.S - p_grp * a.src_per_group);
   int p_s = 0, issued = 0;
-  int4 ent_chunk = make_int4(0, 0, 0, 0);
-  long long chunk_item = -1;
-  int chunk_id = -1;
+  auto load_chunk = [&](int grp, int ns, int base) -> int4 {
+    const int i = base + lane;
+    return i < ns ? __ldg(a.steps + (long long)grp * a.src_per_group + i) : make_int4(0, 0, 0, 0);
+  };
+  int4 ent_chunk = load_chunk(p_grp, p_ns, 0);
   auto issue_one = [&]() {
     // all 32 lanes call this (convergent), lane 0 issues
-    const int grp = (int)(p_item / a.n_tiles);
-    const int j = (int)(p_item % a.n_tiles);
-    const int cid = p_s >> 5;
-    if (p_item != chunk_item || cid != chunk_id) {
-      const int pos = grp * a.src_per_group + cid * 32 + lane;
-      const int ns = mix_group_size(a, p_item);
-      ent_chunk = (cid * 32 + lane < ns) ? a.steps[pos] : make_int4(0, 0, 0, 0);
-      chunk_item = p_item;
-      chunk_id = cid;
-    }
-    int4 ent;
-    ent.x = __shfl_sync(0xffffffffu, ent_chunk.x, p_s & 31);
-    ent.y = __shfl_sync(0xffffffffu, ent_chunk.y, p_s & 31);
-    ent.z = __shfl_sync(0xffffffffu, ent_chunk.z, p_s & 31);
-    ent.w = __shfl_sync(0xffffffffu, ent_chunk.w, p_s & 31);
+    if (p_s > 0 && (p_s & 31) == 0) ent_chunk = load_chunk(p_grp, p_ns, p_s);
+    const int src = __shfl_sync(0xffffffffu, ent_chunk.x, p_s & 31);
+    const int dir = __shfl_sync(0xffffffffu, ent_chunk.y, p_s & 31);
+    const int flags = __shfl_sync(0xffffffffu, ent_chunk.z | (ent_chunk.w << 1), p_s & 31);
     if (lane == 0) {
       const int stage = issued % kMixStages;
       float* tile = wbase + stage * L.stage_floats;
-      int2* taps = reinterpret_cast<int2*>(tile + L.taps_off);
-      const int src = ent.x, dir = ent.y, last = ent.w;
-      const long long w0 = (long long)j * kW + slice_sig0;  // signal index of slice[0]
-      const long long lo = max(w0, 0LL), hi = min(w0 + L.slice, a.T);
-      const int n = (int)max(hi - lo, 0LL);
-      const int nb = n & ~3;
+      const int last = flags >> 1;
+      const long long w0 = (long long)p_j * kW + slice_sig0;  // signal index of slice[0]
       const float* y = a.y + (long long)src * a.y_pitch;
-      for (long long i = 0; i < lo - w0 && i < L.slice; ++i) tile[i] = 0.f;
-      for (int i = nb; i < n; ++i) tile[(lo - w0) + i] = __ldg(y + lo + i);
-      for (long long i = max(lo - w0, 0LL) + n; i < L.slice; ++i) tile[i] = 0.f;
-      *reinterpret_cast<int4*>(tile + L.meta_off) = make_int4(ent.z, ent.w, dir, src);
+      int nb;
+      if (w0 >= 0 && w0 + SLICE <= a.T) {
+        nb = SLICE & ~3;
+        for (int i = nb; i < SLICE; ++i) tile[i] = __ldg(y + w0 + i);
+      } else {  // signal edges: zero padding
+        const long long lo = max(w0, 0LL), hi = min(w0 + SLICE, a.T);
+        const int n = (int)max(hi - lo, 0LL);
+        nb = n & ~3;
+        for (int i = 0; i < SLICE; ++i) {
+          const long long t = w0 + i;
+          if (t < lo || t >= lo + nb) tile[i] = (t >= 0 && t < a.T) ? __ldg(y + t) : 0.f;
+        }
+      }
+      const long long lo = max(w0, 0LL);
+      *reinterpret_cast<int4*>(tile + L.meta_off) = make_int4(flags & 1, last, dir, src);
       const unsigned tap_bytes = last ? 2u * a.tap_stride * 8u : 0u;
       mbar_arrive_expect_tx(&full[stage], (unsigned)nb * 4u + tap_bytes);
       if (nb) bulk_load(tile + (lo - w0), y + lo, (unsigned)nb * 4u, &full[stage]);
       if (last) {
+        int2* taps = reinterpret_cast<int2*>(tile + L.taps_off);
         for (int e = 0; e < 2; ++e) {
           const int ee = e < a.ears ? e : 0;
           bulk_load(taps + e * a.tap_stride, a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride,
@@ -235,21 +240,40 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       }
     }
     ++issued;
-    if (++p_s >= mix_group_size(a, p_item)) {
+    if (++p_s == p_ns) {
       p_s = 0;
-      ++p_item;
+      if (++p_j == a.n_tiles) {
+        p_j = 0;
+        ++p_grp;
+        p_ns = p_grp < a.groups ? min(a.src_per_group, a.S - p_grp * a.src_per_group) : 0;
+      }
+      if (p_ns > 0) ent_chunk = load_chunk(p_grp, p_ns, 0);
     }
   };
   long long total = 0;
-  for (long long it = it0; it < it1; ++it) total += mix_group_size(a, it);
+  {
+    int g = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)g * a.n_tiles);
+    for (long long it = it0; it < it1; ++it) {
+      total += min(a.src_per_group, a.S - g * a.src_per_group);
+      if (++j == a.n_tiles) {
+        j = 0;
+        ++g;
+      }
+    }
+  }
   while (issued < min((long long)kMixStages - 1, total)) issue_one();
 
-  int step = 0;
+  int step = 0, stage = 0;
+  unsigned phase = 0;
+  int c_grp = (int)(it0 / a.n_tiles), c_j = (int)(it0 - (long long)c_grp * a.n_tiles);
   for (long long item = it0; item < it1; ++item) {
-    const int j = (int)(item % a.n_tiles);
-    const int grp = (int)(item / a.n_tiles);
+    const int j = c_j, grp = c_grp;
+    if (++c_j == a.n_tiles) {
+      c_j = 0;
+      ++c_grp;
+    }
     const long long T0 = (long long)j * kW;
-    const int ns = mix_group_size(a, item);
+    const int ns = min(a.src_per_group, a.S - grp * a.src_per_group);
     float accA[16], accB[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
@@ -258,30 +282,34 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
     }
     for (int s = 0; s < ns; ++s, ++step) {
       if (issued < total) issue_one();  // refills the stage this warp released last step
-      const int stage = step % kMixStages;
-      mbar_wait(&full[stage], (unsigned)((step / kMixStages) & 1));
+      mbar_wait(&full[stage], phase);
       const float* tile = wbase + stage * L.stage_floats;
+      if (++stage == kMixStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
       const int4 meta = *reinterpret_cast<const int4*>(tile + L.meta_off);
       if (s == 0) {  // the previous item's bulk store may still be reading acc_tile
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
       }
-      // sum this direction's sources over the warp's slice (coalesced, conflict-free);
-      // a direction with a single source reads its window straight from the stage
-      const float* win = (meta.x && meta.y) ? tile : acc_tile;
-      if (meta.x && meta.y) {
-      } else if (meta.x) {
-        for (int i = 4 * lane; i < L.slice; i += 128)
-          *reinterpret_cast<float4*>(&acc_tile[i]) = *reinterpret_cast<const float4*>(&tile[i]);
+      // sum this direction's sources over the warp's slice into a bank-padded
+      // accumulator (coalesced, conflict-free), so that the per-lane window
+      // reads below (lane stride 16 floats) are conflict-free too
+      if (meta.x) {
+#pragma unroll
+        for (int i = 4 * lane; i < SLICE; i += 128)
+          *reinterpret_cast<float4*>(&acc_tile[padi(i)]) = *reinterpret_cast<const float4*>(&tile[i]);
       } else {
-        for (int i = 4 * lane; i < L.slice; i += 128) {
-          float4 acc4 = *reinterpret_cast<const float4*>(&acc_tile[i]);
+#pragma unroll
+        for (int i = 4 * lane; i < SLICE; i += 128) {
+          float4 acc4 = *reinterpret_cast<const float4*>(&acc_tile[padi(i)]);
           const float4 t4 = *reinterpret_cast<const float4*>(&tile[i]);
           acc4.x += t4.x;
           acc4.y += t4.y;
           acc4.z += t4.z;
           acc4.w += t4.w;
-          *reinterpret_cast<float4*>(&acc_tile[i]) = acc4;
+          *reinterpret_cast<float4*>(&acc_tile[padi(i)]) = acc4;
         }
       }
       __syncwarp();
@@ -293,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
           float v[16];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 t4 = *reinterpret_cast<const float4*>(&win[16 * lane + c + 4 * q]);
+            const float4 t4 = *reinterpret_cast<const float4*>(&acc_tile[padi(16 * lane + c + 4 * q)]);
             v[4 * q] = t4.x;
             v[4 * q + 1] = t4.y;
             v[4 * q + 2] = t4.z;
@@ -328,9 +356,9 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
           }
           const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
 #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            accA[r] = fmaf(va, XA[r], accA[r]);
-            accB[r] = fmaf(vb, XB[r], accB[r]);
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
           }
           ta = tan;
           tb = tbn;
@@ -351,9 +379,9 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
           const float va = k < nA ? __int_as_float(ta.y) : 0.f;
           const float vb = k < nB ? __int_as_float(tb.y) : 0.f;
 #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            accA[r] = fmaf(va, XA[r], accA[r]);
-            accB[r] = fmaf(vb, XB[r], accB[r]);
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
           }
         }
       }
@@ -418,6 +446,347 @@ cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st
     case 112: return mix_nnz<112>(a, sm_count, st);
     case 240: return mix_nnz<240>(a, sm_count, st);
     case 496: return mix_nnz<496>(a, sm_count, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------ bucketed mix ----
+// One pass over the sources, no intermediate per-direction sums in HBM.
+// Item = (group of buckets, tile of 2048 z samples); persistent CTAs walk a
+// contiguous item range.  Per bucket (all sources of one direction):
+//   1. every thread sums its 4-sample columns of the bucket's sources over the
+//      tile window x[T0-128, T0+2048) straight from HBM into registers (float4
+//      loads, two sources in flight), then stores the sum into a bank-padded
+//      shared tile;
+//   2. each lane writes its 16+KWIN window into its TMEM lane row;
+//   3. both ears' taps run as one interleaved pair of TMEM-load/FFMA2 chains,
+//      accumulating the item's z tile in registers.
+// 4 CTAs per SM (TMEM 128 columns each) overlap one CTA's loads with the
+// others' tap loops.  The item's partial leaves by bulk store.
+#ifndef TOEP_MIXB_WADDR
+#define TOEP_MIXB_WADDR 0
+#endif
+#ifndef TOEP_MIXB_FADD2
+#define TOEP_MIXB_FADD2 1
+#endif
+template <int KWIN>
+struct MixBCfg {
+  static constexpr int COLS = kR + KWIN;
+  static constexpr int TILE = kW + COLS;            // window samples of a tile (x[T0 - COLS, T0 + kW))
+  static constexpr int V4 = (TILE / 4 + kThreads - 1) / kThreads;  // float4 columns per thread
+  static constexpr int SLOTS = 3;                   // prefetched source tiles per bucket (cp.async)
+  static constexpr int SLOT_STRIDE = 4 * kThreads * V4;
+};
+constexpr int kMixBMaxBuckets = 512;   // buckets per group (shared-memory tables)
+constexpr int kMixBGroupSrcs = 2048;   // source indices of a group kept in shared memory
+
+struct MixBLayout {
+  int tile_off, slot_off, taps_off, bptr_off, bdir_off, bsrc_off, total_bytes;
+};
+
+__host__ __device__ inline MixBLayout mixb_layout(int KWIN, int tap_stride) {
+  MixBLayout L{};
+  const int tile = kW + kR + KWIN;
+  const int v4 = (tile / 4 + kThreads - 1) / kThreads;
+  L.tile_off = 0;
+  int off = (padded_len(tile) + 31) & ~31;
+  L.slot_off = off;  // [SLOTS][kThreads * V4] float4, thread-private columns
+  off += 3 * 4 * kThreads * v4;
+  L.taps_off = off;  // [2][tap_stride] int2
+  off += (4 * tap_stride + 3) & ~3;
+  L.bptr_off = off;
+  off += kMixBMaxBuckets + 4;
+  L.bdir_off = off;
+  off += kMixBMaxBuckets;
+  L.bsrc_off = off;
+  off += kMixBGroupSrcs;
+  L.total_bytes = off * 4;
+  return L;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int KWIN, int NNZT>
+__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixb(MixBArgs a) {
+  using C = MixBCfg<KWIN>;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ unsigned s_tbase;
+  const MixBLayout L = mixb_layout(KWIN, a.tap_stride);
+  float* s_tile = smem + L.tile_off;  // padded [TILE]
+  float4* s_slot = reinterpret_cast<float4*>(smem + L.slot_off);
+  int2* s_taps = reinterpret_cast<int2*>(smem + L.taps_off);
+  int* s_bptr = reinterpret_cast<int*>(smem + L.bptr_off);
+  int* s_bdir = reinterpret_cast<int*>(smem + L.bdir_off);
+  int* s_bsrc = reinterpret_cast<int*>(smem + L.bsrc_off);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) tmem_alloc<C::COLS>(&s_tbase);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
+
+  const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
+  const long long it0 = (long long)blockIdx.x * per;
+  const long long it1 = min(a.n_items, it0 + per);
+  int grp = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)grp * a.n_tiles);
+  int tab_grp = -1, gfirst = 0;
+  bool src_in_smem = false;
+  float chk0 = 0.f, chk1 = 0.f;  // v*0 accumulates NaN iff some summed sample was inf/NaN
+  for (long long item = it0; item < it1; ++item) {
+    const int b0 = grp * a.buckets_per_group, nb = min(a.buckets - b0, a.buckets_per_group);
+    if (grp != tab_grp) {  // the group's bucket tables -> shared memory
+      __syncthreads();
+      for (int i = tid; i <= nb; i += kThreads) s_bptr[i] = __ldg(a.bptr + b0 + i);
+      for (int i = tid; i < nb; i += kThreads) s_bdir[i] = __ldg(a.bdir + b0 + i);
+      gfirst = __ldg(a.bptr + b0);
+      const int gn = __ldg(a.bptr + b0 + nb) - gfirst;
+      src_in_smem = gn <= kMixBGroupSrcs;
+      if (src_in_smem)
+        for (int i = tid; i < gn; i += kThreads) s_bsrc[i] = __ldg(a.bsrc + gfirst + i);
+      __syncthreads();
+      tab_grp = grp;
+    }
+    auto src_at = [&](int i) { return src_in_smem ? s_bsrc[i - gfirst] : __ldg(a.bsrc + i); };
+    const long long T0 = (long long)j * kW;
+    const long long x0 = T0 - C::COLS;  // signal index of s_tile[0]
+    const bool interior = x0 >= 0 && x0 + C::TILE <= a.T;
+    // this thread's float4 columns of bucket k's first SLOTS sources -> its slots
+    auto prefetch = [&](int k) {
+      const int i0 = s_bptr[k], n = min(s_bptr[k + 1] - i0, C::SLOTS);
+      for (int u = 0; u < n; ++u) {
+        const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i0 + u) * a.y_pitch + x0);
+#pragma unroll
+        for (int q = 0; q < C::V4; ++q) {
+          const int c = tid + q * kThreads;
+          if (c < C::TILE / 4) cp_async16(&s_slot[u * (kThreads * C::V4) + c], ys + c);
+        }
+      }
+      cp_async_commit();
+    };
+    float accA[16], accB[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      accA[r] = 0.f;
+      accB[r] = 0.f;
+    }
+    if (interior && nb > 0) prefetch(0);
+    for (int k = 0; k < nb; ++k) {
+      const int i0 = s_bptr[k], i1 = s_bptr[k + 1];
+      const int dir = s_bdir[k];
+      // ---- 1. bucket sum over the tile window -> registers ------------------
+      float4 v[C::V4];
+#pragma unroll
+      for (int q = 0; q < C::V4; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (interior) {
+        cp_async_wait_all();
+        const int n = min(i1 - i0, C::SLOTS);
+        for (int u = 0; u < n; ++u) {
+#pragma unroll
+          for (int q = 0; q < C::V4; ++q) {
+            const int c = tid + q * kThreads;
+            if (c < C::TILE / 4) {
+              const float4 l = s_slot[u * (kThreads * C::V4) + c];
+#if TOEP_MIXB_FADD2
+              fadd2(v[q].x, v[q].y, l.x, l.y);
+              fadd2(v[q].z, v[q].w, l.z, l.w);
+#else
+              v[q].x += l.x;
+              v[q].y += l.y;
+              v[q].z += l.z;
+              v[q].w += l.w;
+#endif
+            }
+          }
+        }
+        for (int i = i0 + C::SLOTS; i < i1; ++i) {  // large buckets: the rest straight from HBM
+          const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i) * a.y_pitch + x0);
+#pragma unroll
+          for (int q = 0; q < C::V4; ++q) {
+            const int c = tid + q * kThreads;
+            if (c < C::TILE / 4) {
+              const float4 l = __ldcs(ys + c);
+              v[q].x += l.x;
+              v[q].y += l.y;
+              v[q].z += l.z;
+              v[q].w += l.w;
+            }
+          }
+        }
+      } else {  // signal edges: scalar loads with zero padding
+        for (int i = i0; i < i1; ++i) {
+          const float* ys = a.y + (long long)src_at(i) * a.y_pitch;
+#pragma unroll
+          for (int q = 0; q < C::V4; ++q) {
+            const int c = tid + q * kThreads;
+            if (c < C::TILE / 4) {
+              const long long t = x0 + 4 * c;
+              v[q].x += (t >= 0 && t < a.T) ? ys[t] : 0.f;
+              v[q].y += (t + 1 >= 0 && t + 1 < a.T) ? ys[t + 1] : 0.f;
+              v[q].z += (t + 2 >= 0 && t + 2 < a.T) ? ys[t + 2] : 0.f;
+              v[q].w += (t + 3 >= 0 && t + 3 < a.T) ? ys[t + 3] : 0.f;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < C::V4; ++q) {
+        ffma2(chk0, chk1, v[q].x, v[q].y, 0.f);
+        ffma2(chk0, chk1, v[q].z, v[q].w, 0.f);
+      }
+      __syncthreads();  // every warp finished the previous bucket's window write
+      {
+        float* tb = s_tile + padi(4 * tid);  // padi(4*(tid + 128q)) = padi(4*tid) + 576q
+#pragma unroll
+        for (int q = 0; q < C::V4; ++q)
+          if (tid + q * kThreads < C::TILE / 4) *reinterpret_cast<float4*>(tb + 576 * q) = v[q];
+      }
+      for (int i = tid; i < 2 * a.tap_stride; i += kThreads) {
+        const int e = i >= a.tap_stride, kk = i - e * a.tap_stride;
+        const int ee = e < a.ears ? e : 0;
+        s_taps[i] = __ldg(a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride + kk);
+      }
+      __syncthreads();
+      if (interior && k + 1 < nb) prefetch(k + 1);  // next bucket's loads overlap this bucket's taps
+      // ---- 2. lane windows -> TMEM -----------------------------------------
+      {
+        // lane window = s_tile[padi(w0 + m)], w0 = 16 + 16*row, m = 0..COLS-1.  With
+        // p = w0 & 16: padi(w0 + m) = padi(w0) + m + 4*(m >> 5) + (p && (m & 16) ? 4 : 0),
+        // i.e. two base pointers and compile-time offsets (no per-load index math).
+        const int w0 = 16 * tid + 16;
+        const float* wb0 = s_tile + padi(w0);
+        const float* wb1 = wb0 + ((w0 & 16) ? 4 : 0);
+#pragma unroll
+        for (int c = 0; c < C::COLS; c += 16) {
+          float w[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int m = c + 4 * q;
+#if TOEP_MIXB_WADDR
+            const float4 t4 = *reinterpret_cast<const float4*>(((m & 16) ? wb1 : wb0) + m + 4 * (m >> 5));
+#else
+            const float4 t4 = *reinterpret_cast<const float4*>(&s_tile[padi(w0 + m)]);
+#endif
+            w[4 * q] = t4.x;
+            w[4 * q + 1] = t4.y;
+            w[4 * q + 2] = t4.z;
+            w[4 * q + 3] = t4.w;
+          }
+          tmem_st16(tlane + c, w);
+        }
+        tmem_wait_st();
+      }
+      // ---- 3. both ears' taps ----------------------------------------------
+      const int2* tA = s_taps;
+      const int2* tB = s_taps + a.tap_stride;
+      const float keepB = a.ears > 1 ? 1.f : 0.f;
+      if constexpr (NNZT > 0) {
+        float XA0[16], XB0[16], XA1[16], XB1[16];
+        int2 ta = tA[0], tb = tB[0];
+        int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
+        tmem_ld16(XA0, tlane + ta.x);
+        tmem_ld16(XB0, tlane + tb.x);
+#pragma unroll
+        for (int k = 0; k < NNZT; ++k) {
+          const int2 tann = tA[k + 2 < NNZT ? k + 2 : NNZT - 1];
+          const int2 tbnn = tB[k + 2 < NNZT ? k + 2 : NNZT - 1];
+          float(&XA)[16] = (k & 1) ? XA1 : XA0;
+          float(&XB)[16] = (k & 1) ? XB1 : XB0;
+          float(&YA)[16] = (k & 1) ? XA0 : XA1;
+          float(&YB)[16] = (k & 1) ? XB0 : XB1;
+          const unsigned na = tlane + tan.x, nb = tlane + tbn.x;
+          tmem_wait_ld();
+          if (k + 1 < NNZT) {
+            tmem_ld16(YA, na);
+            tmem_ld16(YB, nb);
+          }
+          const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
+          }
+          ta = tan;
+          tb = tbn;
+          tan = tann;
+          tbn = tbnn;
+        }
+      } else {
+        const int nA = __ldg(a.row_nnz + dir);
+        const int nB = a.ears > 1 ? __ldg(a.row_nnz + a.dirs + dir) : 0;
+        const int nk = max(nA, nB);
+        for (int k = 0; k < nk; ++k) {
+          const int2 ta = tA[k], tb = tB[k];
+          float XA[16], XB[16];
+          tmem_ld16(XA, tlane + ta.x);
+          tmem_ld16(XB, tlane + tb.x);
+          tmem_wait_ld();
+          const float va = k < nA ? __int_as_float(ta.y) : 0.f;
+          const float vb = k < nB ? __int_as_float(tb.y) : 0.f;
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
+          }
+        }
+      }
+    }
+    // ---- the group's partial for this tile (once per item: plain stores) ----
+    const long long out_col = T0 + (long long)warp * 32 * kR + 16 * lane;
+    if (out_col < a.zlen) {
+      float4* pA = reinterpret_cast<float4*>(a.part + (long long)grp * a.ears * a.part_pitch + out_col);
+#pragma unroll
+      for (int r = 0; r < 16; r += 4) pA[r / 4] = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
+      if (a.ears > 1) {
+        float4* pB = reinterpret_cast<float4*>(a.part + ((long long)grp * a.ears + 1) * a.part_pitch + out_col);
+#pragma unroll
+        for (int r = 0; r < 16; r += 4) pB[r / 4] = make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
+      }
+    }
+    if (++j == a.n_tiles) {
+      j = 0;
+      ++grp;
+    }
+  }
+  const bool bad = !isfinite(chk0 + chk1);
+  if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<C::COLS>(s_tbase);
+}
+
+template <int KWIN, int NNZT>
+static cudaError_t launch_mixb_t(const MixBArgs& a, int sm_count, cudaStream_t st) {
+  const int bytes = mixb_layout(KWIN, a.tap_stride).total_bytes;
+  auto kern = k_mixb<KWIN, NNZT>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err != cudaSuccess) return err;
+  long long grid = (long long)sm_count * (512 / (kR + KWIN));  // TMEM-bounded co-residency
+  if (grid > a.n_items) grid = a.n_items;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, kThreads, bytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int KWIN>
+static cudaError_t mixb_nnz(const MixBArgs& a, int nnz_uniform, int sm, cudaStream_t st) {
+  switch (nnz_uniform) {
+    case 8: return launch_mixb_t<KWIN, 8>(a, sm, st);
+    case 16: return launch_mixb_t<KWIN, 16>(a, sm, st);
+    case 24: return launch_mixb_t<KWIN, 24>(a, sm, st);
+    case 32: return launch_mixb_t<KWIN, 32>(a, sm, st);
+    default: return launch_mixb_t<KWIN, 0>(a, sm, st);
+  }
+}
+
+cudaError_t launch_mixb(const MixBArgs& a, int kwin, int nnz_uniform, int sm_count, cudaStream_t st) {
+  switch (kwin) {
+    case 112: return mixb_nnz<112>(a, nnz_uniform, sm_count, st);
+    case 240: return mixb_nnz<240>(a, nnz_uniform, sm_count, st);
+    case 496: return mixb_nnz<496>(a, nnz_uniform, sm_count, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -109,6 +109,32 @@ struct MixArgs {
 };
 cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st);
 
+// Bucketed mix (one pass over the sources): buckets are the sets of sources
+// sharing a direction; item = (bucket group, 2048-sample tile).
+struct MixBArgs {
+  const float* y;        // sources, row s at y + s * y_pitch, length T
+  long long T;
+  long long y_pitch;
+  const int* bsrc;       // sources ordered by bucket
+  const int* bptr;       // [buckets + 1]
+  const int* bdir;       // [buckets] direction of each bucket
+  int buckets;
+  int buckets_per_group;
+  int groups;
+  int n_tiles;           // ceil(zlen / 2048)
+  long long n_items;     // groups * n_tiles
+  const int2* taps;      // ear-major [ears * dirs][tap_stride], col = KWIN - o
+  const int* row_nnz;
+  int tap_stride;
+  int dirs;
+  int ears;
+  float* part;           // [groups][ears][part_pitch]
+  long long part_pitch;
+  long long zlen;        // T + K - 1
+  int* nonfinite;        // set to 1 when a non-finite source sample is read (may be null)
+};
+cudaError_t launch_mixb(const MixBArgs& a, int kwin, int nnz_uniform, int sm_count, cudaStream_t st);
+
 // yb[b] = sum of the sources bsrc[bptr[b] .. bptr[b+1]) (all of one direction).
 cudaError_t launch_bucket_sum(const float* y, long long y_pitch, long long T, const int* bsrc, const int* bptr,
                               int buckets, float* yb, long long yb_pitch, int sm_count, cudaStream_t st);

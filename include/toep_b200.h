@@ -84,6 +84,14 @@ int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny);
  * ref: Renderer.render (engine/__init__.py:238-260) for all directions. */
 int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, float* out, int64_t out_pitch,
                          void* stream);
+/* Fused input check (the reference's DataError "signal contains non-finite
+ * samples", engine/__init__.py:162-165): every render / reflect / mixer /
+ * streamer kernel made from this renderer ORs a device flag when it reads an
+ * inf or NaN input sample (no extra pass over the input).  This call waits
+ * for `stream`, returns the flag in *nonfinite (0/1) and clears it;
+ * nonfinite == NULL only clears it (stream-ordered, no wait).
+ * (Reflection lengths > 497 take the banded fallback, which is not covered.) */
+int toep_renderer_check(const toep_renderer* r, int32_t* nonfinite, void* stream);
 /* Stage 2 only, rows [row0, row0+nrows) of one ear against a precomputed
  * y*f (length nyf): the per-direction reflection convolution of
  * Renderer.render once the resonance cache is warm (engine/__init__.py:252-260). */

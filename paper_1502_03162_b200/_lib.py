@@ -24,7 +24,7 @@ EXPORTS = (
     "toep_conv_dense", "toep_conv_sparse",
     "toep_taps_create", "toep_taps_destroy", "toep_taps_info", "toep_taps_conv",
     "toep_renderer_create", "toep_renderer_destroy", "toep_renderer_out_len", "toep_renderer_min_pitch",
-    "toep_renderer_render", "toep_renderer_reflect",
+    "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check",
     "toep_mixer_create", "toep_mixer_destroy", "toep_mixer_z_len", "toep_mixer_out_len",
     "toep_mixer_partial", "toep_mixer_finish",
     "toep_streamer_create", "toep_streamer_destroy", "toep_streamer_reset", "toep_streamer_step",
@@ -75,6 +75,7 @@ def load_library(path: str = LIB_PATH):
         "toep_renderer_min_pitch": (_i64, [_vp, _i64]),
         "toep_renderer_render": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
         "toep_renderer_reflect": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp, _i64, _vp]),
+        "toep_renderer_check": (ctypes.c_int, [_vp, _i32p, _vp]),
         "toep_mixer_create": (ctypes.c_int, [_vp, _i32p, _i32, _i64, ctypes.POINTER(_vp)]),
         "toep_mixer_destroy": (ctypes.c_int, [_vp]),
         "toep_mixer_z_len": (_i64, [_vp]),
@@ -213,6 +214,15 @@ class NativeRenderer:
     def render(self, y, out, pitch: int, stream=None):
         check(load_library().toep_renderer_render(self._h, dptr(y), int(y.numel()), dptr(out), int(pitch),
                                                   stream_ptr(stream)))
+
+    def clear_nonfinite(self, stream=None):
+        check(load_library().toep_renderer_check(self._h, None, stream_ptr(stream)))
+
+    def nonfinite(self, stream=None) -> bool:
+        """Waits for the stream; True if a kernel of this renderer read an inf/NaN input since the last call."""
+        flag = ctypes.c_int32(0)
+        check(load_library().toep_renderer_check(self._h, ctypes.byref(flag), stream_ptr(stream)))
+        return bool(flag.value)
 
     def reflect(self, ear: int, yf, out, pitch: int, stream=None):
         check(load_library().toep_renderer_reflect(self._h, int(ear), dptr(yf), int(yf.numel()), dptr(out),

@@ -68,6 +68,9 @@ class _ModelSet:
         self.taps = _lib.Taps(self.rows, self.K)
         self.native = _lib.NativeRenderer(f, self.taps, self.dirs)
         self.M = self.lf + self.K - 1
+        # non-finite inputs are detected inside the kernels (a device flag, no
+        # extra pass) on every path except the banded fallback for K > 497
+        self.fused_check = self.K <= 497
 
 
 class BatchRenderer(_ModelSet):
@@ -99,8 +102,11 @@ class BatchRenderer(_ModelSet):
             x = t.from_numpy(np.ascontiguousarray(getattr(y, "samples", y), dtype=np.float32)).to("cuda")
         if x.ndim != 1 or x.numel() == 0:
             raise DataError("signal must be a non-empty 1-d array")
-        if check_finite and not bool(t.isfinite(x).all()):
+        fused_check = check_finite and self.fused_check
+        if check_finite and not fused_check and not bool(t.isfinite(x).all()):
             raise DataError("signal contains non-finite samples")
+        if fused_check:
+            self.native.clear_nonfinite(stream)
         ny = x.numel()
         if out is None:
             out = self.alloc(ny)
@@ -112,6 +118,8 @@ class BatchRenderer(_ModelSet):
         if pitch < self.out_len(ny):
             raise DataError("output pitch %d < %d samples" % (pitch, self.out_len(ny)))
         self.native.render(x, out, pitch, stream)
+        if fused_check and self.native.nonfinite(stream):
+            raise DataError("signal contains non-finite samples")
         self.counters["resonance_macs"] += self.ears * self.lf * ny
         self.counters["reflection_macs"] += int(self.row_nnz.sum()) * (ny + self.lf - 1)
         self.counters["calls"] += 1
@@ -153,8 +161,11 @@ class MixRenderer(_ModelSet):
         t = _lib.require_cuda()
         return t.zeros((self.ears, (self.z_len + 3) // 4 * 4), device="cuda", dtype=t.float32)
 
-    def partial(self, y, s0: int = 0, count: int | None = None, z=None, stream=None):
-        """z[e] = sum over sources [s0, s0+count) of y_s * g_{e,dir(s)}; y row i is source s0+i."""
+    def partial(self, y, s0: int = 0, count: int | None = None, z=None, stream=None, check_finite: bool = True):
+        """z[e] = sum over sources [s0, s0+count) of y_s * g_{e,dir(s)}; y row i is source s0+i.
+
+        ``check_finite`` raises DataError (after the launch; the check is fused
+        into the kernel's source reads) if any source sample is inf or NaN."""
         t = _lib.require_cuda()
         count = self.S - s0 if count is None else int(count)
         if y.dim() != 2 or y.shape[0] < count or y.shape[1] < self.T or y.stride(1) != 1:
@@ -163,7 +174,11 @@ class MixRenderer(_ModelSet):
             raise DataError("sources must be float32 CUDA tensors")
         if z is None:
             z = self.alloc_z()
+        if check_finite:
+            self.native.clear_nonfinite(stream)
         self.mixer.partial(y, y.stride(0), s0, count, z, z.stride(0), stream)
+        if check_finite and self.native.nonfinite(stream):
+            raise DataError("signal contains non-finite samples")
         return z
 
     def finish(self, z, out=None, stream=None):
@@ -173,8 +188,8 @@ class MixRenderer(_ModelSet):
         self.mixer.finish(z, z.stride(0), out, out.stride(0), stream)
         return out[:, : self.out_len]
 
-    def render(self, y, stream=None):
-        return self.finish(self.partial(y, stream=stream), stream=stream)
+    def render(self, y, stream=None, check_finite: bool = True):
+        return self.finish(self.partial(y, stream=stream, check_finite=check_finite), stream=stream)
 
 
 class StreamRenderer(_ModelSet):
@@ -192,6 +207,12 @@ class StreamRenderer(_ModelSet):
 
     def reset(self, stream=None):
         self.streamer.reset(stream)
+        self.native.clear_nonfinite(stream)
+
+    def nonfinite(self, stream=None) -> bool:
+        """True if any block since the last reset/query held an inf or NaN sample
+        (flag set inside the step kernel; this call waits for the stream)."""
+        return self.native.nonfinite(stream)
 
     def step(self, block, out=None, stream=None):
         t = _lib.require_cuda()

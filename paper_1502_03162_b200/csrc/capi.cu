@@ -192,7 +192,7 @@ int toep_taps_info(const toep_taps* t, int32_t* rows, int32_t* length, int32_t* 
 // all reading the same input signal x (nx samples).  `pairs`/`pnnz` are the
 // rows' pair-interleaved taps (k_pair_taps); null -> built here for this call.
 static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pairs, const int4* pnnz, const float* x,
-                        long long nx, float* out, long long out_pitch, cudaStream_t st) {
+                        long long nx, float* out, long long out_pitch, cudaStream_t st, int* nonfinite = nullptr) {
   const long long out_len = nx + t->length - 1;
   if (t->kwin > 0) {
     if (!aligned16(out) || (nrows > 1 && out_pitch % 4 != 0))
@@ -229,6 +229,7 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pai
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;
+    a.nonfinite = nonfinite;
     RenderMaps maps;
     cudaError_t e = make_render_maps(out, nrows, out_len, out_pitch, &maps);
     if (e == cudaSuccess) e = launch_render(a, maps, t->kwin, false, sm_count_cached(), st);
@@ -388,6 +389,21 @@ int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny) {
   return r ? round_up(toep_renderer_out_len(r, ny), 4) : -1;
 }
 
+int toep_renderer_check(const toep_renderer* r, int32_t* nonfinite, void* stream) {
+  if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
+  cudaStream_t st = S(stream);
+  if (!nonfinite) {  // clear only (stream-ordered, no wait)
+    TOEP_CUDA(cudaMemsetAsync(r->d_nonfinite, 0, sizeof(int), st));
+    return TOEP_OK;
+  }
+  int h = 0;
+  TOEP_CUDA(cudaMemcpyAsync(&h, r->d_nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TOEP_CUDA(cudaMemsetAsync(r->d_nonfinite, 0, sizeof(int), st));
+  TOEP_CUDA(cudaStreamSynchronize(st));
+  *nonfinite = h;
+  return TOEP_OK;
+}
+
 int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, float* out, int64_t out_pitch,
                          void* stream) {
   if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
@@ -419,6 +435,7 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;
+    a.nonfinite = r->d_nonfinite;
     RenderMaps maps;
     cudaError_t e = make_render_maps(out, rows, out_len, out_pitch, &maps);
     if (e != cudaSuccess) return cuda_fail(e, "tensor map (output rows)");
@@ -462,7 +479,8 @@ int toep_renderer_reflect(const toep_renderer* r, int32_t ear, const float* yf, 
   if (r->dirs > 1 && out_pitch < nyf + r->g->length - 1) return fail(TOEP_ERR_INVALID, "output pitch too small");
   const int4* pairs = r->d_pairs ? r->d_pairs + (size_t)ear * r->pairs_per_ear * r->g->tap_stride : nullptr;
   const int4* pnnz = r->d_pnnz ? r->d_pnnz + (size_t)ear * r->pairs_per_ear : nullptr;
-  return reflect_rows(r->g, ear * r->dirs, r->dirs, pairs, pnnz, yf, nyf, out, out_pitch, S(stream));
+  return reflect_rows(r->g, ear * r->dirs, r->dirs, pairs, pnnz, yf, nyf, out, out_pitch, S(stream),
+                      r->d_nonfinite);
 }
 
 }  // extern "C"
@@ -824,6 +842,7 @@ int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch
   a.out_pitch = s->r->ears > 1 ? out_pitch : s->B;
   a.ctas = s->ctas;
   a.ticket = s->d_ticket;
+  a.nonfinite = s->r->d_nonfinite;
   cudaError_t e = launch_stream_step(a, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "launch_stream_step");
   return TOEP_OK;

@@ -900,13 +900,18 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
   float* s_w = sm;                                                // [ns][L]
   int2* s_tap = reinterpret_cast<int2*>(sm + a.src_per_cta * L);  // [ns][ears][tap_stride]
   int* s_nnz = reinterpret_cast<int*>(s_tap + a.src_per_cta * a.ears * a.tap_stride);
+  float chk = 0.f;  // fused DataError check on the new block's samples
   {
     const int q4 = L / 4, h4 = a.H / 4;
     for (int i = tid; i < ns * q4; i += blockDim.x) {
       const int s = i / q4, q = i - s * q4;
       float4 v;
-      if (q < h4) v = *reinterpret_cast<const float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q);
-      else v = __ldg(reinterpret_cast<const float4*>(a.block + (long long)(s0 + s) * a.block_pitch) + (q - h4));
+      if (q < h4) {
+        v = *reinterpret_cast<const float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q);
+      } else {
+        v = __ldg(reinterpret_cast<const float4*>(a.block + (long long)(s0 + s) * a.block_pitch) + (q - h4));
+        chk = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, chk))));
+      }
       *reinterpret_cast<float4*>(&s_w[s * L + 4 * q]) = v;
     }
     for (int i = tid; i < ns * a.ears * a.tap_stride; i += blockDim.x) {
@@ -937,6 +942,7 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     a.part[((long long)blockIdx.x * a.ears) * a.B + t] = acc0;
     if (a.ears > 1) a.part[((long long)blockIdx.x * a.ears + 1) * a.B + t] = acc1;
   }
+  if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk)) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
   // roll the sources' history: keep the last H samples of [hist | block]
   for (int i = tid; i < ns * (a.H / 4); i += blockDim.x) {
     const int s = i / (a.H / 4), q = i - s * (a.H / 4);

@@ -34,6 +34,7 @@ struct RenderArgs {
   float* out;            // row r at out + r * out_pitch
   long long out_pitch;   // floats, multiple of 4, >= n_tiles*2048 rounded down to 512 granularity
   long long out_len;
+  int* nonfinite;        // set to 1 when a non-finite input sample is read (may be null)
 };
 
 // TMA tensor maps over the output rows ([rows][out_len], row stride out_pitch):
@@ -168,6 +169,7 @@ struct StreamArgs {
   long long out_pitch;
   int ctas;
   unsigned int* ticket;  // [ceil(ctas/16) + 1] zero-initialised counters owned by the stream state
+  int* nonfinite;        // set to 1 when a non-finite input sample is read (may be null)
 };
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st);
 

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
   float* st = smem + L.region_off + warp * (kStageFloatsPerWarp * kWarps / NW);
   const int half = lane >> 4, inner = (lane & 15) * 16;
 
+  float chk = 0.f;  // x*0 accumulates NaN iff an input sample was inf/NaN (fused DataError check)
   for (long long u = u0; u < u1;) {
     int e, j, dd0;
     um.decode(u, e, j, dd0);
@@ -201,7 +202,9 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
       const long long xs = T0 - C::YH - a.lf_pad;  // signal index of s_x[0]
       for (int i = tid; i < xlen; i += NT) {
         const long long t = xs + i;
-        s_x[padi(i)] = (t >= 0 && t < a.nx) ? __ldg(a.x + t) : 0.f;
+        const float v = (t >= 0 && t < a.nx) ? __ldg(a.x + t) : 0.f;
+        chk = fmaf(v, 0.f, chk);
+        s_x[padi(i)] = v;
       }
       if (reuse_halo)  // last YH values of the previous tile are this tile's halo
         for (int i = tid; i < C::YH; i += NT) s_yf[i] = s_halo[i];
@@ -232,7 +235,9 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
       const long long xs = T0 - C::YH;
       for (int i = tid; i < kW + C::YH; i += NT) {
         const long long t = xs + i;
-        s_yf[i] = (t >= 0 && t < a.nx) ? __ldg(xe + t) : 0.f;
+        const float v = (t >= 0 && t < a.nx) ? __ldg(xe + t) : 0.f;
+        chk = fmaf(v, 0.f, chk);
+        s_yf[i] = v;
       }
     }
     __syncthreads();
@@ -431,6 +436,7 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
     }
     chunk_base += nchunks;
   }
+  if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
   if (lane == 0) bulk_wait_all();
   tmem_fence_before();
   __syncthreads();

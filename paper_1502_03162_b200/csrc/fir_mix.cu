@@ -758,10 +758,282 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixb(MixBArgs a
   if (warp == 0) tmem_dealloc<C::COLS>(s_tbase);
 }
 
+// ------------------------------------------------- warp-private variant ----
+// Same items and buckets as k_mixb, but every warp runs its own pipeline on
+// its 512-output quarter: it sums its (512 + KWIN)-sample slice of each source
+// (22% halo re-read, HBM is not the binding limit here), writes its lanes'
+// windows from a warp-private padded slice, and prefetches the next bucket's
+// sources *and* tap rows with cp.async.  No CTA barrier inside the bucket
+// loop (only when the group's tables change), so warps drift freely.
+constexpr int kMixWGroupSrcs = 1024;
+
+struct MixWLayout {
+  int warp_floats, slice_off, slot_off, taps_off, bptr_off, bdir_off, bsrc_off, total_bytes;
+};
+
+__host__ __device__ inline MixWLayout mixw_layout(int KWIN, int tap_stride) {
+  MixWLayout L{};
+  const int slice = 32 * kR + KWIN;
+  const int v4 = (slice / 4 + 31) / 32;
+  L.slice_off = 0;  // padded [slice]
+  int off = (padded_len(slice) + 31) & ~31;
+  L.slot_off = off;  // [SLOTS][32 lanes * v4] float4 (lane-private)
+  off += 3 * 4 * 32 * v4;
+  L.taps_off = off;  // [2 buffers][2 ears][tap_stride] int2
+  off += 2 * 2 * 2 * tap_stride;
+  L.warp_floats = (off + 31) & ~31;
+  off = kWarps * L.warp_floats;
+  L.bptr_off = off;
+  off += kMixBMaxBuckets + 4;
+  L.bdir_off = off;
+  off += kMixBMaxBuckets;
+  L.bsrc_off = off;
+  off += kMixWGroupSrcs;
+  L.total_bytes = off * 4;
+  return L;
+}
+
+template <int KWIN, int NNZT>
+__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a) {
+  constexpr int COLS = kR + KWIN;
+  constexpr int SLICE = 32 * kR + KWIN;
+  constexpr int V4 = (SLICE / 4 + 31) / 32;
+  constexpr int SLOTS = 3;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ unsigned s_tbase;
+  const MixWLayout L = mixw_layout(KWIN, a.tap_stride);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* wb = smem + warp * L.warp_floats;
+  float* s_slice = wb + L.slice_off;
+  float4* s_slot = reinterpret_cast<float4*>(wb + L.slot_off);
+  int2* s_taps = reinterpret_cast<int2*>(wb + L.taps_off);
+  int* s_bptr = reinterpret_cast<int*>(smem + L.bptr_off);
+  int* s_bdir = reinterpret_cast<int*>(smem + L.bdir_off);
+  int* s_bsrc = reinterpret_cast<int*>(smem + L.bsrc_off);
+  if (warp == 0) tmem_alloc<COLS>(&s_tbase);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
+
+  const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
+  const long long it0 = (long long)blockIdx.x * per;
+  const long long it1 = min(a.n_items, it0 + per);
+  int grp = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)grp * a.n_tiles);
+  int tab_grp = -1, gfirst = 0;
+  bool src_in_smem = false;
+  float chk0 = 0.f, chk1 = 0.f;
+  for (long long item = it0; item < it1; ++item) {
+    const int b0 = grp * a.buckets_per_group, nb = min(a.buckets - b0, a.buckets_per_group);
+    if (grp != tab_grp) {  // the group's bucket tables -> shared memory (all warps at this item)
+      __syncthreads();
+      for (int i = tid; i <= nb; i += kThreads) s_bptr[i] = __ldg(a.bptr + b0 + i);
+      for (int i = tid; i < nb; i += kThreads) s_bdir[i] = __ldg(a.bdir + b0 + i);
+      gfirst = __ldg(a.bptr + b0);
+      const int gn = __ldg(a.bptr + b0 + nb) - gfirst;
+      src_in_smem = gn <= kMixWGroupSrcs;
+      if (src_in_smem)
+        for (int i = tid; i < gn; i += kThreads) s_bsrc[i] = __ldg(a.bsrc + gfirst + i);
+      __syncthreads();
+      tab_grp = grp;
+    }
+    auto src_at = [&](int i) { return src_in_smem ? s_bsrc[i - gfirst] : __ldg(a.bsrc + i); };
+    const long long T0 = (long long)j * kW;
+    const long long w0 = T0 + (long long)warp * 32 * kR - KWIN;  // signal index of s_slice[0]
+    const bool interior = w0 >= 0 && w0 + SLICE <= a.T;
+    auto prefetch = [&](int k) {  // bucket k's first SLOTS sources (lane columns) and its two tap rows
+      const int i0 = s_bptr[k], n = min(s_bptr[k + 1] - i0, SLOTS);
+      if (interior) {
+        for (int u = 0; u < n; ++u) {
+          const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i0 + u) * a.y_pitch + w0);
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            const int c = lane + 32 * q;
+            if (c < SLICE / 4) cp_async16(&s_slot[u * 32 * V4 + c], ys + c);
+          }
+        }
+      }
+      const int dir = s_bdir[k];
+      int2* tb = s_taps + (k & 1) * 2 * a.tap_stride;
+      for (int i = lane; i < a.tap_stride; i += 32) {  // 2 taps (16 B) per copy
+        const int e = i >= a.tap_stride / 2, kk = 2 * (i - e * (a.tap_stride / 2));
+        const int ee = e < a.ears ? e : 0;
+        cp_async16(tb + e * a.tap_stride + kk, a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride + kk);
+      }
+      cp_async_commit();
+    };
+    float accA[16], accB[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      accA[r] = 0.f;
+      accB[r] = 0.f;
+    }
+    if (nb > 0) prefetch(0);
+    for (int k = 0; k < nb; ++k) {
+      const int i0 = s_bptr[k], i1 = s_bptr[k + 1];
+      float4 v[V4];
+#pragma unroll
+      for (int q = 0; q < V4; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      cp_async_wait_all();
+      if (interior) {
+        const int n = min(i1 - i0, SLOTS);
+        for (int u = 0; u < n; ++u) {
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            const int c = lane + 32 * q;
+            if (c < SLICE / 4) {
+              const float4 l = s_slot[u * 32 * V4 + c];
+              fadd2(v[q].x, v[q].y, l.x, l.y);
+              fadd2(v[q].z, v[q].w, l.z, l.w);
+            }
+          }
+        }
+        for (int i = i0 + SLOTS; i < i1; ++i) {
+          const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i) * a.y_pitch + w0);
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            const int c = lane + 32 * q;
+            if (c < SLICE / 4) {
+              const float4 l = __ldcs(ys + c);
+              fadd2(v[q].x, v[q].y, l.x, l.y);
+              fadd2(v[q].z, v[q].w, l.z, l.w);
+            }
+          }
+        }
+      } else {
+        for (int i = i0; i < i1; ++i) {
+          const float* ys = a.y + (long long)src_at(i) * a.y_pitch;
+#pragma unroll
+          for (int q = 0; q < V4; ++q) {
+            const int c = lane + 32 * q;
+            if (c < SLICE / 4) {
+              const long long t = w0 + 4 * c;
+              v[q].x += (t >= 0 && t < a.T) ? ys[t] : 0.f;
+              v[q].y += (t + 1 >= 0 && t + 1 < a.T) ? ys[t + 1] : 0.f;
+              v[q].z += (t + 2 >= 0 && t + 2 < a.T) ? ys[t + 2] : 0.f;
+              v[q].w += (t + 3 >= 0 && t + 3 < a.T) ? ys[t + 3] : 0.f;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < V4; ++q) {
+        ffma2(chk0, chk1, v[q].x, v[q].y, 0.f);
+        ffma2(chk0, chk1, v[q].z, v[q].w, 0.f);
+      }
+      __syncwarp();  // previous bucket's window reads of s_slice are done; tap rows of k visible
+      {
+        float* sb = s_slice + padi(4 * lane);  // padi(4*(lane + 32q)) = padi(4*lane) + 144q
+#pragma unroll
+        for (int q = 0; q < V4; ++q)
+          if (lane + 32 * q < SLICE / 4) *reinterpret_cast<float4*>(sb + 144 * q) = v[q];
+      }
+      __syncwarp();
+      const int2* tA = s_taps + (k & 1) * 2 * a.tap_stride;
+      const int2* tB = tA + a.tap_stride;
+      const int dir = s_bdir[k];
+      if (k + 1 < nb) prefetch(k + 1);  // next bucket's loads overlap this bucket's taps
+      {
+#pragma unroll
+        for (int c = 0; c < COLS; c += 16) {
+          float w[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 t4 = *reinterpret_cast<const float4*>(&s_slice[padi(16 * lane + c + 4 * q)]);
+            w[4 * q] = t4.x;
+            w[4 * q + 1] = t4.y;
+            w[4 * q + 2] = t4.z;
+            w[4 * q + 3] = t4.w;
+          }
+          tmem_st16(tlane + c, w);
+        }
+        tmem_wait_st();
+      }
+      const float keepB = a.ears > 1 ? 1.f : 0.f;
+      if constexpr (NNZT > 0) {
+        float XA0[16], XB0[16], XA1[16], XB1[16];
+        int2 ta = tA[0], tb = tB[0];
+        int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
+        tmem_ld16(XA0, tlane + ta.x);
+        tmem_ld16(XB0, tlane + tb.x);
+#pragma unroll
+        for (int kk = 0; kk < NNZT; ++kk) {
+          const int2 tann = tA[kk + 2 < NNZT ? kk + 2 : NNZT - 1];
+          const int2 tbnn = tB[kk + 2 < NNZT ? kk + 2 : NNZT - 1];
+          float(&XA)[16] = (kk & 1) ? XA1 : XA0;
+          float(&XB)[16] = (kk & 1) ? XB1 : XB0;
+          float(&YA)[16] = (kk & 1) ? XA0 : XA1;
+          float(&YB)[16] = (kk & 1) ? XB0 : XB1;
+          const unsigned na = tlane + tan.x, nb2 = tlane + tbn.x;
+          tmem_wait_ld();
+          if (kk + 1 < NNZT) {
+            tmem_ld16(YA, na);
+            tmem_ld16(YB, nb2);
+          }
+          const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
+          }
+          ta = tan;
+          tb = tbn;
+          tan = tann;
+          tbn = tbnn;
+        }
+      } else {
+        const int nA = __ldg(a.row_nnz + dir);
+        const int nB = a.ears > 1 ? __ldg(a.row_nnz + a.dirs + dir) : 0;
+        const int nk = max(nA, nB);
+        for (int kk = 0; kk < nk; ++kk) {
+          const int2 ta = tA[kk], tb = tB[kk];
+          float XA[16], XB[16];
+          tmem_ld16(XA, tlane + ta.x);
+          tmem_ld16(XB, tlane + tb.x);
+          tmem_wait_ld();
+          const float va = kk < nA ? __int_as_float(ta.y) : 0.f;
+          const float vb = kk < nB ? __int_as_float(tb.y) : 0.f;
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
+            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
+          }
+        }
+      }
+    }
+    const long long out_col = T0 + (long long)warp * 32 * kR + 16 * lane;
+    if (out_col < a.zlen) {
+      float4* pA = reinterpret_cast<float4*>(a.part + (long long)grp * a.ears * a.part_pitch + out_col);
+#pragma unroll
+      for (int r = 0; r < 16; r += 4) pA[r / 4] = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
+      if (a.ears > 1) {
+        float4* pB = reinterpret_cast<float4*>(a.part + ((long long)grp * a.ears + 1) * a.part_pitch + out_col);
+#pragma unroll
+        for (int r = 0; r < 16; r += 4) pB[r / 4] = make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
+      }
+    }
+    if (++j == a.n_tiles) {
+      j = 0;
+      ++grp;
+    }
+  }
+  cp_async_wait_all();
+  const bool bad = !isfinite(chk0 + chk1);
+  if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<COLS>(s_tbase);
+}
+
 template <int KWIN, int NNZT>
 static cudaError_t launch_mixb_t(const MixBArgs& a, int sm_count, cudaStream_t st) {
-  const int bytes = mixb_layout(KWIN, a.tap_stride).total_bytes;
-  auto kern = k_mixb<KWIN, NNZT>;
+  static const bool warp_private = [] {
+    const char* ev = getenv("TOEP_MIX_KERNEL");
+    return !(ev && ev[0] == 'b');
+  }();
+  const int bytes = warp_private ? mixw_layout(KWIN, a.tap_stride).total_bytes
+                                 : mixb_layout(KWIN, a.tap_stride).total_bytes;
+  auto kern = warp_private ? k_mixw<KWIN, NNZT> : k_mixb<KWIN, NNZT>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   long long grid = (long long)sm_count * (512 / (kR + KWIN));  // TMEM-bounded co-residency

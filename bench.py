@@ -455,7 +455,7 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     tot = _max_over_ranks(sum(ms_steps), world)
     samples = cfg.sources * cfg.ears * T  # src x ear (one direction per source)
     value = samples * args.steps / (tot * 1e-3)
-    # dominant kernel: k_mixb (+ its partial reduce), timed alone with CUDA events
+    # dominant kernel: k_mix (+ its partial reduce), timed alone with CUDA events
     # on the launching stream over a few extra launches after the timed region
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     reps = max(1, min(args.steps, 5))
@@ -479,7 +479,7 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     achieved = bytes_local / (kern_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(workload),
-            "peak_src": "measured", "kernel": "k_mixb<112,24> (+k_mix_reduce)", "kernel_ms": kern_ms,
+            "peak_src": "measured", "kernel": "k_mix<112,24> (+k_mix_reduce)", "kernel_ms": kern_ms,
             "alg_bytes_per_launch": bytes_local, "distinct_directions": int(ndist),
             "fp32_tflops": flops_local / (kern_ms * 1e-3) / 1e12,
             "fp32_frac": flops_local / (kern_ms * 1e-3) / 1e12 / fp32_peak}

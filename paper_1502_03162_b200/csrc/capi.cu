@@ -326,6 +326,7 @@ struct toep_renderer {
   int4* d_pairs = nullptr;   // [ears][pairs_per_ear][tap_stride] pair-interleaved taps (k_render)
   int4* d_pnnz = nullptr;    // [ears][pairs_per_ear]
   int* d_nonfinite = nullptr;  // sticky flag: a kernel read a non-finite input sample
+  int4* d_epairs = nullptr;    // [dirs][tap_stride] ear-interleaved taps (mixdown)
 };
 
 extern "C" {
@@ -362,6 +363,9 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
     if (e == cudaSuccess) e = cudaMalloc(&r->d_pnnz, np * sizeof(int4));
     if (e == cudaSuccess)
       e = launch_pair_taps(g->d_kw, g->d_nnz, ears, dirs, g->tap_stride, g->kwin, r->d_pairs, r->d_pnnz, nullptr);
+    if (e == cudaSuccess && ears <= 2) e = cudaMalloc(&r->d_epairs, (size_t)dirs * g->tap_stride * sizeof(int4));
+    if (e == cudaSuccess && ears <= 2)
+      e = launch_ear_pair_taps(g->d_kw, dirs, ears, g->tap_stride, g->kwin, r->d_epairs, nullptr);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
@@ -376,6 +380,7 @@ int toep_renderer_destroy(toep_renderer* r) {
   if (!r) return TOEP_OK;
   if (r->d_f) cudaFree(r->d_f);
   if (r->d_nonfinite) cudaFree(r->d_nonfinite);
+  if (r->d_epairs) cudaFree(r->d_epairs);
   if (r->d_pairs) cudaFree(r->d_pairs);
   if (r->d_pnnz) cudaFree(r->d_pnnz);
   delete r;
@@ -490,30 +495,15 @@ struct toep_mixer {
   const toep_renderer* r = nullptr;
   int S = 0;
   long long T = 0, zlen = 0;
-  int* d_dir = nullptr;
   std::vector<int> h_dir;
-  int4* d_steps = nullptr;      // direction-sorted step table of the last [s0, s0+count) range
-  int order_s0 = -1, order_count = -1;
-  // same-direction buckets of that range (used when some direction has > 1 source)
+  int order_s0 = -1, order_count = -1;  // source range the bucket tables describe
   int buckets = 0;
-  bool use_buckets = false;
-  int* d_bsrc = nullptr;        // sources sorted by direction
-  int* d_bptr = nullptr;        // bucket b = d_bsrc[d_bptr[b] .. d_bptr[b+1])
-  int* d_bdir = nullptr;        // direction of bucket b
-  int4* d_bsteps = nullptr;     // one step per bucket {b, dir, 1, 1}
-  float* d_yb = nullptr;        // bucket sums [buckets][yb_pitch]
-  size_t yb_bytes = 0;
-  long long yb_pitch = 0;
+  int* d_bsrc = nullptr;  // sources sorted by direction
+  int* d_bptr = nullptr;  // bucket b = d_bsrc[d_bptr[b] .. d_bptr[b+1])
+  int* d_bdir = nullptr;  // direction of bucket b
   float* d_part = nullptr;
   size_t part_bytes = 0;
 };
-
-static constexpr int kSrcPerGroup = 256;
-
-static bool mix_legacy() {
-  const char* ev = getenv("TOEP_MIX_LEGACY");
-  return ev && atoi(ev) != 0;
-}
 
 static cudaError_t ensure_part(toep_mixer* m, size_t need, cudaStream_t st) {
   if (need <= m->part_bytes) return cudaSuccess;
@@ -550,13 +540,9 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
   m->T = T;
   m->zlen = T + r->g->length - 1;
   m->h_dir.assign(src_dir_host, src_dir_host + n_src);
-  cudaError_t e = cudaMalloc(&m->d_dir, n_src * sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&m->d_steps, n_src * sizeof(int4));
-  if (e == cudaSuccess) e = cudaMalloc(&m->d_bsrc, n_src * sizeof(int));
+  cudaError_t e = cudaMalloc(&m->d_bsrc, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bptr, (n_src + 1) * sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&m->d_bsteps, n_src * sizeof(int4));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bdir, n_src * sizeof(int));
-  if (e == cudaSuccess) e = cudaMemcpy(m->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     toep_mixer_destroy(m);
     return cuda_fail(e, "toep_mixer_create");
@@ -567,13 +553,9 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
 
 int toep_mixer_destroy(toep_mixer* m) {
   if (!m) return TOEP_OK;
-  if (m->d_dir) cudaFree(m->d_dir);
-  if (m->d_steps) cudaFree(m->d_steps);
   if (m->d_bsrc) cudaFree(m->d_bsrc);
   if (m->d_bptr) cudaFree(m->d_bptr);
-  if (m->d_bsteps) cudaFree(m->d_bsteps);
   if (m->d_bdir) cudaFree(m->d_bdir);
-  if (m->d_yb) cudaFree(m->d_yb);
   if (m->d_part) cudaFree(m->d_part);
   delete m;
   return TOEP_OK;
@@ -594,33 +576,22 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   cudaStream_t st = S(stream);
   const toep_taps* g = m->r->g;
   if (s0 != m->order_s0 || count != m->order_count) {
-    // stable sort of the range by direction; per sorted position {src, dir, first, last}
-    // within its group: sources sharing a direction are summed before their taps
+    // buckets: stable sort of the range by direction; bucket b = sources
+    // bsrc[bptr[b] .. bptr[b+1]) (indices relative to s0), all at bdir[b]
     std::vector<int> ord(count);
     for (int i = 0; i < count; ++i) ord[i] = i;
     const int* dir = m->h_dir.data() + s0;
     std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
-    std::vector<int4> steps(count);
-    std::vector<int> bptr(1, 0);
-    std::vector<int4> bsteps;
-    std::vector<int> bdir;
+    std::vector<int> bptr(1, 0), bdir;
     for (int p = 0; p < count; ++p) {
-      const int d = dir[ord[p]];
-      const bool first = (p % kSrcPerGroup == 0) || dir[ord[p - 1]] != d;
-      const bool last = ((p + 1) % kSrcPerGroup == 0) || p + 1 == count || dir[ord[p + 1]] != d;
-      steps[p] = make_int4(ord[p], d, first ? 1 : 0, last ? 1 : 0);
-      if (p + 1 == count || dir[ord[p + 1]] != d) {
-        bsteps.push_back(make_int4((int)bsteps.size(), d, 1, 1));
-        bdir.push_back(d);
+      if (p + 1 == count || dir[ord[p + 1]] != dir[ord[p]]) {
+        bdir.push_back(dir[ord[p]]);
         bptr.push_back(p + 1);
       }
     }
-    m->buckets = (int)bsteps.size();
-    m->use_buckets = m->buckets < count;  // some direction holds several sources
-    TOEP_CUDA(cudaMemcpyAsync(m->d_steps, steps.data(), count * sizeof(int4), cudaMemcpyHostToDevice, st));
+    m->buckets = (int)bdir.size();
     TOEP_CUDA(cudaMemcpyAsync(m->d_bsrc, ord.data(), count * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaMemcpyAsync(m->d_bptr, bptr.data(), bptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    TOEP_CUDA(cudaMemcpyAsync(m->d_bsteps, bsteps.data(), bsteps.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaMemcpyAsync(m->d_bdir, bdir.data(), bdir.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaStreamSynchronize(st));
     m->order_s0 = s0;
@@ -628,16 +599,16 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   }
   const int n_tiles = (int)((m->zlen + kW - 1) / kW);
   const long long part_pitch = (long long)n_tiles * kW;
-  if (!mix_legacy()) {
-    // one pass: k_mixb sums each bucket's sources per tile on the fly
+  // one pass: the mix kernel sums each bucket's sources per tile on the fly
+  {
     const int sm = sm_count_cached();
     const long long slots = (long long)sm * (512 / (kR + g->kwin));
     // >= ~24 items per persistent CTA keeps the tail short; fewer groups keep the partials small
     long long bpg = ((long long)m->buckets * n_tiles + 24 * slots - 1) / (24 * slots);
-    bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, 512), m->buckets));  // <= kMixBMaxBuckets
+    bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, 512), m->buckets));  // <= kMixMaxBuckets
     const int groups = (int)((m->buckets + bpg - 1) / bpg);
     TOEP_CUDA(ensure_part(m, (size_t)groups * m->r->ears * part_pitch * sizeof(float), st));
-    MixBArgs a{};
+    MixArgs a{};
     a.y = y;
     a.T = m->T;
     a.y_pitch = count > 1 ? y_pitch : round_up(m->T, 4);
@@ -650,6 +621,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.n_tiles = n_tiles;
     a.n_items = (long long)groups * n_tiles;
     a.taps = g->d_kw;
+    a.etaps = m->r->d_epairs;
     a.row_nnz = g->d_nnz;
     a.tap_stride = g->tap_stride;
     a.dirs = m->r->dirs;
@@ -658,67 +630,12 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.part_pitch = part_pitch;
     a.zlen = m->zlen;
     a.nonfinite = m->r->d_nonfinite;
-    cudaError_t e = launch_mixb(a, g->kwin, g->uniform ? g->max_nnz : 0, sm, st);
-    if (e != cudaSuccess) return cuda_fail(e, "launch_mixb");
+    cudaError_t e = launch_mix(a, g->kwin, g->uniform ? g->max_nnz : 0, sm, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_mix");
     e = launch_mix_reduce(m->d_part, groups, m->r->ears, part_pitch, m->zlen, z, z_pitch, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_mix_reduce");
     return TOEP_OK;
   }
-  // legacy two-pass path (TOEP_MIX_LEGACY=1): per-direction sums in HBM, then k_mix
-  const float* xs = y;
-  long long xs_pitch = y_pitch;
-  int nsteps = count;
-  const int4* steps_dev = m->d_steps;
-  if (m->use_buckets) {
-    const long long pitch = round_up(m->T, 4);
-    const size_t need_b = (size_t)m->buckets * pitch * sizeof(float);
-    if (need_b > m->yb_bytes) {
-      if (m->d_yb) {
-        TOEP_CUDA(cudaStreamSynchronize(st));
-        cudaFree(m->d_yb);
-        m->d_yb = nullptr;
-        m->yb_bytes = 0;
-      }
-      TOEP_CUDA(cudaMalloc(&m->d_yb, need_b));
-      m->yb_bytes = need_b;
-    }
-    m->yb_pitch = pitch;
-    cudaError_t eb = launch_bucket_sum(y, count > 1 ? y_pitch : round_up(m->T, 4), m->T, m->d_bsrc, m->d_bptr,
-                                       m->buckets, m->d_yb, pitch, sm_count_cached(), st);
-    if (eb != cudaSuccess) return cuda_fail(eb, "launch_bucket_sum");
-    xs = m->d_yb;
-    xs_pitch = pitch;
-    nsteps = m->buckets;
-    steps_dev = m->d_bsteps;
-  }
-  const int groups = (nsteps + kSrcPerGroup - 1) / kSrcPerGroup;
-  TOEP_CUDA(ensure_part(m, (size_t)groups * m->r->ears * part_pitch * sizeof(float), st));
-  MixArgs a{};
-  a.y = xs;
-  a.steps = steps_dev;
-  a.T = m->T;
-  a.y_pitch = xs_pitch;
-  a.src_dir = m->d_dir + s0;
-  a.S = nsteps;
-  a.taps = g->d_kw;
-  a.row_nnz = g->d_nnz;
-  a.tap_stride = g->tap_stride;
-  a.uniform_nnz = g->uniform;
-  a.tap_stride_nnz = g->max_nnz;
-  a.dirs = m->r->dirs;
-  a.ears = m->r->ears;
-  a.src_per_group = kSrcPerGroup;
-  a.groups = groups;
-  a.n_tiles = n_tiles;
-  a.n_items = (long long)groups * n_tiles;
-  a.part = m->d_part;
-  a.part_pitch = part_pitch;
-  a.zlen = m->zlen;
-  cudaError_t e = launch_mix(a, g->kwin, sm_count_cached(), st);
-  if (e != cudaSuccess) return cuda_fail(e, "launch_mix");
-  e = launch_mix_reduce(m->d_part, groups, m->r->ears, part_pitch, m->zlen, z, z_pitch, st);
-  if (e != cudaSuccess) return cuda_fail(e, "launch_mix_reduce");
-  return TOEP_OK;
 }
 
 int toep_mixer_finish(const toep_mixer* m, const float* z, int64_t z_pitch, float* out, int64_t out_pitch,

@@ -117,392 +117,25 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// ----------------------------------------------------------- g-first mix ----
-// Work item = (source group, time tile).  Sources are visited in direction-
-// sorted order (a.steps), and the time tiles of all sources that share a
-// direction are summed before any reflection tap is applied:
-//     sum_s y_s * g_{dir(s)} = sum_d g_d * (sum_{s: dir(s)=d} y_s)      (linearity)
-// so the TMEM window write and the 2 x nnz taps run once per *direction*
-// present in the group, not once per source.
-//
-// Every warp is its own pipeline: lane 0 streams the warp's 624-sample slice
-// of each source tile (cp.async.bulk + mbarrier complete_tx) and, on a
-// direction's last source, its two reflection rows into a warp-private
-// kMixStages-deep ring, kMixStages-1 sources ahead; the warp adds slices into
-// a private accumulator and, per direction, writes its lanes' windows into its
-// TMEM lane quarter and runs both ears as one interleaved pair of
-// TMEM-load/FFMA chains.  No CTA-wide barrier in the steady state.  Per-ear
-// accumulators persist across the group and leave once per item (bulk store).
-constexpr int kMixStages = 3;
-constexpr int kMixSlice = 32 * kR + 112;  // floats of a tile one warp reads (KWIN <= 112)
-
-struct MixLayout {
-  int slice, stage_floats, taps_off, meta_off, warp_floats, accum_off, bars_off, total;
-};
-
-__host__ __device__ inline MixLayout mix_layout(int KWIN, int tap_stride) {
-  MixLayout L{};
-  L.slice = 32 * kR + KWIN;                              // lane windows 16l + [0, 16 + KWIN)
-  L.taps_off = (L.slice + 3) & ~3;                        // [2 ears][tap_stride] int2
-  L.meta_off = L.taps_off + 4 * tap_stride;               // int4 {first, last, dir, src}
-  L.stage_floats = (L.meta_off + 4 + 31) & ~31;
-  L.accum_off = kMixStages * L.stage_floats;              // slice sums, then the item's store staging
-  const int acc_floats = padded_len(L.slice);             // bank-padded slice sum
-  L.warp_floats = L.accum_off + ((acc_floats > 2 * 32 * kR ? acc_floats : 2 * 32 * kR) + 31 & ~31);
-  L.bars_off = kWarps * L.warp_floats;                    // [warps][kMixStages] uint64
-  L.total = (L.bars_off + 2 * kWarps * kMixStages) * 4 + 128;
-  return L;
-}
-
-template <int KWIN, int NNZT>
-__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) {
-  constexpr int XH = KWIN + kR;
-  constexpr int COLS = kR + KWIN;
-  extern __shared__ __align__(128) float smem[];
-  __shared__ unsigned s_tbase;
-  const MixLayout L = mix_layout(KWIN, a.tap_stride);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  float* wbase = smem + warp * L.warp_floats;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars_off) + warp * kMixStages;
-  float* acc_tile = wbase + L.accum_off;  // aliases the output staging `st`
-  float* st = acc_tile;
-
-  if (warp == 0) tmem_alloc<COLS>(&s_tbase);
-  if (lane == 0) {
-    for (int i = 0; i < kMixStages; ++i) mbar_init(&full[i], 1);
-    mbar_fence_init();
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
-
-  const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
-  const long long it0 = (long long)blockIdx.x * per;
-  const long long it1 = min(a.n_items, it0 + per);
-  if (it0 >= it1) {
-    tmem_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc<COLS>(s_tbase);
-    return;
-  }
-  constexpr int SLICE = 32 * kR + KWIN;          // == L.slice
-  const int slice_sig0 = 32 * kR * warp - KWIN;  // signal offset of the slice relative to T0
-
-  // ---- producer cursor: (group, tile, position) advanced incrementally; the
-  //      group's step entries are read 32 at a time (one coalesced load per
-  //      warp, prefetched a chunk ahead) and broadcast by shuffle.
-  int p_grp = (int)(it0 / a.n_tiles), p_j = (int)(it0 - (long long)p_grp * a.n_tiles);
-  int p_ns = min(a.src_per_group, a.S - p_grp * a.src_per_group);
-  int p_s = 0, issued = 0;
-  auto load_chunk = [&](int grp, int ns, int base) -> int4 {
-    const int i = base + lane;
-    return i < ns ? __ldg(a.steps + (long long)grp * a.src_per_group + i) : make_int4(0, 0, 0, 0);
-  };
-  int4 ent_chunk = load_chunk(p_grp, p_ns, 0);
-  auto issue_one = [&]() {
-    // all 32 lanes call this (convergent), lane 0 issues
-    if (p_s > 0 && (p_s & 31) == 0) ent_chunk = load_chunk(p_grp, p_ns, p_s);
-    const int src = __shfl_sync(0xffffffffu, ent_chunk.x, p_s & 31);
-    const int dir = __shfl_sync(0xffffffffu, ent_chunk.y, p_s & 31);
-    const int flags = __shfl_sync(0xffffffffu, ent_chunk.z | (ent_chunk.w << 1), p_s & 31);
-    if (lane == 0) {
-      const int stage = issued % kMixStages;
-      float* tile = wbase + stage * L.stage_floats;
-      const int last = flags >> 1;
-      const long long w0 = (long long)p_j * kW + slice_sig0;  // signal index of slice[0]
-      const float* y = a.y + (long long)src * a.y_pitch;
-      int nb;
-      if (w0 >= 0 && w0 + SLICE <= a.T) {
-        nb = SLICE & ~3;
-        for (int i = nb; i < SLICE; ++i) tile[i] = __ldg(y + w0 + i);
-      } else {  // signal edges: zero padding
-        const long long lo = max(w0, 0LL), hi = min(w0 + SLICE, a.T);
-        const int n = (int)max(hi - lo, 0LL);
-        nb = n & ~3;
-        for (int i = 0; i < SLICE; ++i) {
-          const long long t = w0 + i;
-          if (t < lo || t >= lo + nb) tile[i] = (t >= 0 && t < a.T) ? __ldg(y + t) : 0.f;
-        }
-      }
-      const long long lo = max(w0, 0LL);
-      *reinterpret_cast<int4*>(tile + L.meta_off) = make_int4(flags & 1, last, dir, src);
-      const unsigned tap_bytes = last ? 2u * a.tap_stride * 8u : 0u;
-      mbar_arrive_expect_tx(&full[stage], (unsigned)nb * 4u + tap_bytes);
-      if (nb) bulk_load(tile + (lo - w0), y + lo, (unsigned)nb * 4u, &full[stage]);
-      if (last) {
-        int2* taps = reinterpret_cast<int2*>(tile + L.taps_off);
-        for (int e = 0; e < 2; ++e) {
-          const int ee = e < a.ears ? e : 0;
-          bulk_load(taps + e * a.tap_stride, a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride,
-                    (unsigned)a.tap_stride * 8u, &full[stage]);
-        }
-      }
-    }
-    ++issued;
-    if (++p_s == p_ns) {
-      p_s = 0;
-      if (++p_j == a.n_tiles) {
-        p_j = 0;
-        ++p_grp;
-        p_ns = p_grp < a.groups ? min(a.src_per_group, a.S - p_grp * a.src_per_group) : 0;
-      }
-      if (p_ns > 0) ent_chunk = load_chunk(p_grp, p_ns, 0);
-    }
-  };
-  long long total = 0;
-  {
-    int g = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)g * a.n_tiles);
-    for (long long it = it0; it < it1; ++it) {
-      total += min(a.src_per_group, a.S - g * a.src_per_group);
-      if (++j == a.n_tiles) {
-        j = 0;
-        ++g;
-      }
-    }
-  }
-  while (issued < min((long long)kMixStages - 1, total)) issue_one();
-
-  int step = 0, stage = 0;
-  unsigned phase = 0;
-  int c_grp = (int)(it0 / a.n_tiles), c_j = (int)(it0 - (long long)c_grp * a.n_tiles);
-  for (long long item = it0; item < it1; ++item) {
-    const int j = c_j, grp = c_grp;
-    if (++c_j == a.n_tiles) {
-      c_j = 0;
-      ++c_grp;
-    }
-    const long long T0 = (long long)j * kW;
-    const int ns = min(a.src_per_group, a.S - grp * a.src_per_group);
-    float accA[16], accB[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      accA[r] = 0.f;
-      accB[r] = 0.f;
-    }
-    for (int s = 0; s < ns; ++s, ++step) {
-      if (issued < total) issue_one();  // refills the stage this warp released last step
-      mbar_wait(&full[stage], phase);
-      const float* tile = wbase + stage * L.stage_floats;
-      if (++stage == kMixStages) {
-        stage = 0;
-        phase ^= 1u;
-      }
-      const int4 meta = *reinterpret_cast<const int4*>(tile + L.meta_off);
-      if (s == 0) {  // the previous item's bulk store may still be reading acc_tile
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-      }
-      // sum this direction's sources over the warp's slice into a bank-padded
-      // accumulator (coalesced, conflict-free), so that the per-lane window
-      // reads below (lane stride 16 floats) are conflict-free too
-      if (meta.x) {
-#pragma unroll
-        for (int i = 4 * lane; i < SLICE; i += 128)
-          *reinterpret_cast<float4*>(&acc_tile[padi(i)]) = *reinterpret_cast<const float4*>(&tile[i]);
-      } else {
-#pragma unroll
-        for (int i = 4 * lane; i < SLICE; i += 128) {
-          float4 acc4 = *reinterpret_cast<const float4*>(&acc_tile[padi(i)]);
-          const float4 t4 = *reinterpret_cast<const float4*>(&tile[i]);
-          acc4.x += t4.x;
-          acc4.y += t4.y;
-          acc4.z += t4.z;
-          acc4.w += t4.w;
-          *reinterpret_cast<float4*>(&acc_tile[padi(i)]) = acc4;
-        }
-      }
-      __syncwarp();
-      if (!meta.y) continue;
-      // lane windows -> TMEM (previous direction's loads were all waited)
-      {
-#pragma unroll
-        for (int c = 0; c < COLS; c += 16) {
-          float v[16];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 t4 = *reinterpret_cast<const float4*>(&acc_tile[padi(16 * lane + c + 4 * q)]);
-            v[4 * q] = t4.x;
-            v[4 * q + 1] = t4.y;
-            v[4 * q + 2] = t4.z;
-            v[4 * q + 3] = t4.w;
-          }
-          tmem_st16(tlane + c, v);
-        }
-        tmem_wait_st();
-      }
-      const int2* tA = reinterpret_cast<const int2*>(tile + L.taps_off);
-      const int2* tB = tA + a.tap_stride;
-      const float keepB = a.ears > 1 ? 1.f : 0.f;
-      if constexpr (NNZT > 0) {
-        float XA0[16], XB0[16], XA1[16], XB1[16];
-        int2 ta = tA[0], tb = tB[0];
-        int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
-        tmem_ld16(XA0, tlane + ta.x);
-        tmem_ld16(XB0, tlane + tb.x);
-#pragma unroll
-        for (int k = 0; k < NNZT; ++k) {
-          const int2 tann = tA[k + 2 < NNZT ? k + 2 : NNZT - 1];
-          const int2 tbnn = tB[k + 2 < NNZT ? k + 2 : NNZT - 1];
-          float(&XA)[16] = (k & 1) ? XA1 : XA0;
-          float(&XB)[16] = (k & 1) ? XB1 : XB0;
-          float(&YA)[16] = (k & 1) ? XA0 : XA1;
-          float(&YB)[16] = (k & 1) ? XB0 : XB1;
-          const unsigned na = tlane + tan.x, nb = tlane + tbn.x;
-          tmem_wait_ld();
-          if (k + 1 < NNZT) {
-            tmem_ld16(YA, na);
-            tmem_ld16(YB, nb);
-          }
-          const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
-#pragma unroll
-          for (int r = 0; r < 16; r += 2) {
-            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
-            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
-          }
-          ta = tan;
-          tb = tbn;
-          tan = tann;
-          tbn = tbnn;
-        }
-      } else {
-        const int dir = meta.z;
-        const int nA = a.row_nnz[dir];
-        const int nB = a.ears > 1 ? a.row_nnz[a.dirs + dir] : 0;
-        const int nk = max(nA, nB);
-        for (int k = 0; k < nk; ++k) {
-          const int2 ta = tA[k], tb = tB[k];
-          float XA[16], XB[16];
-          tmem_ld16(XA, tlane + ta.x);
-          tmem_ld16(XB, tlane + tb.x);
-          tmem_wait_ld();
-          const float va = k < nA ? __int_as_float(ta.y) : 0.f;
-          const float vb = k < nB ? __int_as_float(tb.y) : 0.f;
-#pragma unroll
-          for (int r = 0; r < 16; r += 2) {
-            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
-            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
-          }
-        }
-      }
-      __syncwarp();
-    }
-    // ---- the group's partial for this tile -------------------------------
-    const long long out_col = T0 + (long long)warp * 32 * kR;
-    if (out_col < a.zlen) {
-#pragma unroll
-      for (int r = 0; r < 16; r += 4) {
-        *reinterpret_cast<float4*>(&st[lane * 16 + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
-        *reinterpret_cast<float4*>(&st[512 + lane * 16 + r]) =
-            make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (elect_one()) {
-        for (int e = 0; e < a.ears; ++e)
-          bulk_store(a.part + ((long long)grp * a.ears + e) * a.part_pitch + out_col, st + 512 * e, 32 * kR * 4);
-      }
-    }
-  }
-  if (lane == 0) bulk_wait_all();
-  tmem_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc<COLS>(s_tbase);
-}
-
-template <int KWIN, int NNZT>
-static cudaError_t launch_mix_t(const MixArgs& a, int sm_count, cudaStream_t st) {
-  const int bytes = mix_layout(KWIN, a.tap_stride).total;
-  auto kern = k_mix<KWIN, NNZT>;  // 4 warps, one TMEM lane quarter each
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (err != cudaSuccess) return err;
-  // TMEM bounds co-residency (512 / COLS CTAs per SM); shared memory and
-  // registers are sized to allow exactly that many.
-  int per_sm = 512 / (kR + KWIN);
-  if (getenv("TOEP_MIX_PERSM")) per_sm = atoi(getenv("TOEP_MIX_PERSM"));
-  long long grid = (long long)sm_count * per_sm;
-  if (grid > a.n_items) grid = a.n_items;
-  if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kThreads, bytes, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <int KWIN>
-static cudaError_t mix_nnz(const MixArgs& a, int sm, cudaStream_t st) {
-  if (a.uniform_nnz) {
-    switch (a.tap_stride_nnz) {
-      case 8: return launch_mix_t<KWIN, 8>(a, sm, st);
-      case 16: return launch_mix_t<KWIN, 16>(a, sm, st);
-      case 24: return launch_mix_t<KWIN, 24>(a, sm, st);
-      case 32: return launch_mix_t<KWIN, 32>(a, sm, st);
-      default: break;
-    }
-  }
-  return launch_mix_t<KWIN, 0>(a, sm, st);
-}
-
-cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st) {
-  switch (kwin) {
-    case 112: return mix_nnz<112>(a, sm_count, st);
-    case 240: return mix_nnz<240>(a, sm_count, st);
-    case 496: return mix_nnz<496>(a, sm_count, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-// ------------------------------------------------------ bucketed mix ----
-// One pass over the sources, no intermediate per-direction sums in HBM.
-// Item = (group of buckets, tile of 2048 z samples); persistent CTAs walk a
-// contiguous item range.  Per bucket (all sources of one direction):
-//   1. every thread sums its 4-sample columns of the bucket's sources over the
-//      tile window x[T0-128, T0+2048) straight from HBM into registers (float4
-//      loads, two sources in flight), then stores the sum into a bank-padded
-//      shared tile;
+// --------------------------------------------------------- mixdown ----
+// One pass over the sources; no intermediate per-direction sums in HBM.
+// Buckets are the sets of sources sharing a direction (host stable sort).
+// Item = (group of buckets, 2048-sample z tile); persistent CTAs (4 per SM,
+// TMEM 128 columns each) walk contiguous item ranges, the group's bucket
+// tables sit in shared memory.  Every warp runs its own pipeline on its
+// 512-output quarter of the tile, per bucket (all sources of one direction):
+//   1. sum its (512 + KWIN)-sample slice of the bucket's sources into
+//      registers (the first 3 sources were prefetched with cp.async into
+//      lane-private shared-memory slots while the previous bucket's taps ran;
+//      the rest stream straight from HBM), store the sum into a warp-private
+//      bank-padded slice;
 //   2. each lane writes its 16+KWIN window into its TMEM lane row;
-//   3. both ears' taps run as one interleaved pair of TMEM-load/FFMA2 chains,
-//      accumulating the item's z tile in registers.
-// 4 CTAs per SM (TMEM 128 columns each) overlap one CTA's loads with the
-// others' tap loops.  The item's partial leaves by bulk store.
-#ifndef TOEP_MIXB_WADDR
-#define TOEP_MIXB_WADDR 0
-#endif
-#ifndef TOEP_MIXB_FADD2
-#define TOEP_MIXB_FADD2 1
-#endif
-template <int KWIN>
-struct MixBCfg {
-  static constexpr int COLS = kR + KWIN;
-  static constexpr int TILE = kW + COLS;            // window samples of a tile (x[T0 - COLS, T0 + kW))
-  static constexpr int V4 = (TILE / 4 + kThreads - 1) / kThreads;  // float4 columns per thread
-  static constexpr int SLOTS = 3;                   // prefetched source tiles per bucket (cp.async)
-  static constexpr int SLOT_STRIDE = 4 * kThreads * V4;
-};
-constexpr int kMixBMaxBuckets = 512;   // buckets per group (shared-memory tables)
-constexpr int kMixBGroupSrcs = 2048;   // source indices of a group kept in shared memory
-
-struct MixBLayout {
-  int tile_off, slot_off, taps_off, bptr_off, bdir_off, bsrc_off, total_bytes;
-};
-
-__host__ __device__ inline MixBLayout mixb_layout(int KWIN, int tap_stride) {
-  MixBLayout L{};
-  const int tile = kW + kR + KWIN;
-  const int v4 = (tile / 4 + kThreads - 1) / kThreads;
-  L.tile_off = 0;
-  int off = (padded_len(tile) + 31) & ~31;
-  L.slot_off = off;  // [SLOTS][kThreads * V4] float4, thread-private columns
-  off += 3 * 4 * kThreads * v4;
-  L.taps_off = off;  // [2][tap_stride] int2
-  off += (4 * tap_stride + 3) & ~3;
-  L.bptr_off = off;
-  off += kMixBMaxBuckets + 4;
-  L.bdir_off = off;
-  off += kMixBMaxBuckets;
-  L.bsrc_off = off;
-  off += kMixBGroupSrcs;
-  L.total_bytes = off * 4;
-  return L;
-}
+//   3. both ears' taps (ear-interleaved int4 table, prefetched with the
+//      sources) run as one interleaved pair of TMEM-load/FFMA2 chains,
+//      accumulating the item's z quarter in registers.
+// No CTA barrier inside the bucket loop (only when the group's tables
+// change), so warps drift freely; partials leave once per item.
+constexpr int kMixMaxBuckets = 512;   // buckets per group (shared-memory tables)
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -510,303 +143,49 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int KWIN, int NNZT>
-__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixb(MixBArgs a) {
-  using C = MixBCfg<KWIN>;
-  extern __shared__ __align__(128) float smem[];
-  __shared__ unsigned s_tbase;
-  const MixBLayout L = mixb_layout(KWIN, a.tap_stride);
-  float* s_tile = smem + L.tile_off;  // padded [TILE]
-  float4* s_slot = reinterpret_cast<float4*>(smem + L.slot_off);
-  int2* s_taps = reinterpret_cast<int2*>(smem + L.taps_off);
-  int* s_bptr = reinterpret_cast<int*>(smem + L.bptr_off);
-  int* s_bdir = reinterpret_cast<int*>(smem + L.bdir_off);
-  int* s_bsrc = reinterpret_cast<int*>(smem + L.bsrc_off);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (warp == 0) tmem_alloc<C::COLS>(&s_tbase);
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
 
-  const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
-  const long long it0 = (long long)blockIdx.x * per;
-  const long long it1 = min(a.n_items, it0 + per);
-  int grp = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)grp * a.n_tiles);
-  int tab_grp = -1, gfirst = 0;
-  bool src_in_smem = false;
-  float chk0 = 0.f, chk1 = 0.f;  // v*0 accumulates NaN iff some summed sample was inf/NaN
-  for (long long item = it0; item < it1; ++item) {
-    const int b0 = grp * a.buckets_per_group, nb = min(a.buckets - b0, a.buckets_per_group);
-    if (grp != tab_grp) {  // the group's bucket tables -> shared memory
-      __syncthreads();
-      for (int i = tid; i <= nb; i += kThreads) s_bptr[i] = __ldg(a.bptr + b0 + i);
-      for (int i = tid; i < nb; i += kThreads) s_bdir[i] = __ldg(a.bdir + b0 + i);
-      gfirst = __ldg(a.bptr + b0);
-      const int gn = __ldg(a.bptr + b0 + nb) - gfirst;
-      src_in_smem = gn <= kMixBGroupSrcs;
-      if (src_in_smem)
-        for (int i = tid; i < gn; i += kThreads) s_bsrc[i] = __ldg(a.bsrc + gfirst + i);
-      __syncthreads();
-      tab_grp = grp;
-    }
-    auto src_at = [&](int i) { return src_in_smem ? s_bsrc[i - gfirst] : __ldg(a.bsrc + i); };
-    const long long T0 = (long long)j * kW;
-    const long long x0 = T0 - C::COLS;  // signal index of s_tile[0]
-    const bool interior = x0 >= 0 && x0 + C::TILE <= a.T;
-    // this thread's float4 columns of bucket k's first SLOTS sources -> its slots
-    auto prefetch = [&](int k) {
-      const int i0 = s_bptr[k], n = min(s_bptr[k + 1] - i0, C::SLOTS);
-      for (int u = 0; u < n; ++u) {
-        const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i0 + u) * a.y_pitch + x0);
-#pragma unroll
-        for (int q = 0; q < C::V4; ++q) {
-          const int c = tid + q * kThreads;
-          if (c < C::TILE / 4) cp_async16(&s_slot[u * (kThreads * C::V4) + c], ys + c);
-        }
-      }
-      cp_async_commit();
-    };
-    float accA[16], accB[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      accA[r] = 0.f;
-      accB[r] = 0.f;
-    }
-    if (interior && nb > 0) prefetch(0);
-    for (int k = 0; k < nb; ++k) {
-      const int i0 = s_bptr[k], i1 = s_bptr[k + 1];
-      const int dir = s_bdir[k];
-      // ---- 1. bucket sum over the tile window -> registers ------------------
-      float4 v[C::V4];
-#pragma unroll
-      for (int q = 0; q < C::V4; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (interior) {
-        cp_async_wait_all();
-        const int n = min(i1 - i0, C::SLOTS);
-        for (int u = 0; u < n; ++u) {
-#pragma unroll
-          for (int q = 0; q < C::V4; ++q) {
-            const int c = tid + q * kThreads;
-            if (c < C::TILE / 4) {
-              const float4 l = s_slot[u * (kThreads * C::V4) + c];
-#if TOEP_MIXB_FADD2
-              fadd2(v[q].x, v[q].y, l.x, l.y);
-              fadd2(v[q].z, v[q].w, l.z, l.w);
-#else
-              v[q].x += l.x;
-              v[q].y += l.y;
-              v[q].z += l.z;
-              v[q].w += l.w;
-#endif
-            }
-          }
-        }
-        for (int i = i0 + C::SLOTS; i < i1; ++i) {  // large buckets: the rest straight from HBM
-          const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i) * a.y_pitch + x0);
-#pragma unroll
-          for (int q = 0; q < C::V4; ++q) {
-            const int c = tid + q * kThreads;
-            if (c < C::TILE / 4) {
-              const float4 l = __ldcs(ys + c);
-              v[q].x += l.x;
-              v[q].y += l.y;
-              v[q].z += l.z;
-              v[q].w += l.w;
-            }
-          }
-        }
-      } else {  // signal edges: scalar loads with zero padding
-        for (int i = i0; i < i1; ++i) {
-          const float* ys = a.y + (long long)src_at(i) * a.y_pitch;
-#pragma unroll
-          for (int q = 0; q < C::V4; ++q) {
-            const int c = tid + q * kThreads;
-            if (c < C::TILE / 4) {
-              const long long t = x0 + 4 * c;
-              v[q].x += (t >= 0 && t < a.T) ? ys[t] : 0.f;
-              v[q].y += (t + 1 >= 0 && t + 1 < a.T) ? ys[t + 1] : 0.f;
-              v[q].z += (t + 2 >= 0 && t + 2 < a.T) ? ys[t + 2] : 0.f;
-              v[q].w += (t + 3 >= 0 && t + 3 < a.T) ? ys[t + 3] : 0.f;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < C::V4; ++q) {
-        ffma2(chk0, chk1, v[q].x, v[q].y, 0.f);
-        ffma2(chk0, chk1, v[q].z, v[q].w, 0.f);
-      }
-      __syncthreads();  // every warp finished the previous bucket's window write
-      {
-        float* tb = s_tile + padi(4 * tid);  // padi(4*(tid + 128q)) = padi(4*tid) + 576q
-#pragma unroll
-        for (int q = 0; q < C::V4; ++q)
-          if (tid + q * kThreads < C::TILE / 4) *reinterpret_cast<float4*>(tb + 576 * q) = v[q];
-      }
-      for (int i = tid; i < 2 * a.tap_stride; i += kThreads) {
-        const int e = i >= a.tap_stride, kk = i - e * a.tap_stride;
-        const int ee = e < a.ears ? e : 0;
-        s_taps[i] = __ldg(a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride + kk);
-      }
-      __syncthreads();
-      if (interior && k + 1 < nb) prefetch(k + 1);  // next bucket's loads overlap this bucket's taps
-      // ---- 2. lane windows -> TMEM -----------------------------------------
-      {
-        // lane window = s_tile[padi(w0 + m)], w0 = 16 + 16*row, m = 0..COLS-1.  With
-        // p = w0 & 16: padi(w0 + m) = padi(w0) + m + 4*(m >> 5) + (p && (m & 16) ? 4 : 0),
-        // i.e. two base pointers and compile-time offsets (no per-load index math).
-        const int w0 = 16 * tid + 16;
-        const float* wb0 = s_tile + padi(w0);
-        const float* wb1 = wb0 + ((w0 & 16) ? 4 : 0);
-#pragma unroll
-        for (int c = 0; c < C::COLS; c += 16) {
-          float w[16];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int m = c + 4 * q;
-#if TOEP_MIXB_WADDR
-            const float4 t4 = *reinterpret_cast<const float4*>(((m & 16) ? wb1 : wb0) + m + 4 * (m >> 5));
-#else
-            const float4 t4 = *reinterpret_cast<const float4*>(&s_tile[padi(w0 + m)]);
-#endif
-            w[4 * q] = t4.x;
-            w[4 * q + 1] = t4.y;
-            w[4 * q + 2] = t4.z;
-            w[4 * q + 3] = t4.w;
-          }
-          tmem_st16(tlane + c, w);
-        }
-        tmem_wait_st();
-      }
-      // ---- 3. both ears' taps ----------------------------------------------
-      const int2* tA = s_taps;
-      const int2* tB = s_taps + a.tap_stride;
-      const float keepB = a.ears > 1 ? 1.f : 0.f;
-      if constexpr (NNZT > 0) {
-        float XA0[16], XB0[16], XA1[16], XB1[16];
-        int2 ta = tA[0], tb = tB[0];
-        int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
-        tmem_ld16(XA0, tlane + ta.x);
-        tmem_ld16(XB0, tlane + tb.x);
-#pragma unroll
-        for (int k = 0; k < NNZT; ++k) {
-          const int2 tann = tA[k + 2 < NNZT ? k + 2 : NNZT - 1];
-          const int2 tbnn = tB[k + 2 < NNZT ? k + 2 : NNZT - 1];
-          float(&XA)[16] = (k & 1) ? XA1 : XA0;
-          float(&XB)[16] = (k & 1) ? XB1 : XB0;
-          float(&YA)[16] = (k & 1) ? XA0 : XA1;
-          float(&YB)[16] = (k & 1) ? XB0 : XB1;
-          const unsigned na = tlane + tan.x, nb = tlane + tbn.x;
-          tmem_wait_ld();
-          if (k + 1 < NNZT) {
-            tmem_ld16(YA, na);
-            tmem_ld16(YB, nb);
-          }
-          const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
-#pragma unroll
-          for (int r = 0; r < 16; r += 2) {
-            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
-            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
-          }
-          ta = tan;
-          tb = tbn;
-          tan = tann;
-          tbn = tbnn;
-        }
-      } else {
-        const int nA = __ldg(a.row_nnz + dir);
-        const int nB = a.ears > 1 ? __ldg(a.row_nnz + a.dirs + dir) : 0;
-        const int nk = max(nA, nB);
-        for (int k = 0; k < nk; ++k) {
-          const int2 ta = tA[k], tb = tB[k];
-          float XA[16], XB[16];
-          tmem_ld16(XA, tlane + ta.x);
-          tmem_ld16(XB, tlane + tb.x);
-          tmem_wait_ld();
-          const float va = k < nA ? __int_as_float(ta.y) : 0.f;
-          const float vb = k < nB ? __int_as_float(tb.y) : 0.f;
-#pragma unroll
-          for (int r = 0; r < 16; r += 2) {
-            ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
-            ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
-          }
-        }
-      }
-    }
-    // ---- the group's partial for this tile (once per item: plain stores) ----
-    const long long out_col = T0 + (long long)warp * 32 * kR + 16 * lane;
-    if (out_col < a.zlen) {
-      float4* pA = reinterpret_cast<float4*>(a.part + (long long)grp * a.ears * a.part_pitch + out_col);
-#pragma unroll
-      for (int r = 0; r < 16; r += 4) pA[r / 4] = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
-      if (a.ears > 1) {
-        float4* pB = reinterpret_cast<float4*>(a.part + ((long long)grp * a.ears + 1) * a.part_pitch + out_col);
-#pragma unroll
-        for (int r = 0; r < 16; r += 4) pB[r / 4] = make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
-      }
-    }
-    if (++j == a.n_tiles) {
-      j = 0;
-      ++grp;
-    }
-  }
-  const bool bad = !isfinite(chk0 + chk1);
-  if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
-  tmem_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc<C::COLS>(s_tbase);
-}
+constexpr int kMixGroupSrcs = 1024;
 
-// ------------------------------------------------- warp-private variant ----
-// Same items and buckets as k_mixb, but every warp runs its own pipeline on
-// its 512-output quarter: it sums its (512 + KWIN)-sample slice of each source
-// (22% halo re-read, HBM is not the binding limit here), writes its lanes'
-// windows from a warp-private padded slice, and prefetches the next bucket's
-// sources *and* tap rows with cp.async.  No CTA barrier inside the bucket
-// loop (only when the group's tables change), so warps drift freely.
-constexpr int kMixWGroupSrcs = 1024;
-
-struct MixWLayout {
+struct MixLayout {
   int warp_floats, slice_off, slot_off, taps_off, bptr_off, bdir_off, bsrc_off, total_bytes;
 };
 
-__host__ __device__ inline MixWLayout mixw_layout(int KWIN, int tap_stride) {
-  MixWLayout L{};
+__host__ __device__ inline MixLayout mix_layout(int KWIN, int tap_stride) {
+  MixLayout L{};
   const int slice = 32 * kR + KWIN;
   const int v4 = (slice / 4 + 31) / 32;
   L.slice_off = 0;  // padded [slice]
   int off = (padded_len(slice) + 31) & ~31;
   L.slot_off = off;  // [SLOTS][32 lanes * v4] float4 (lane-private)
   off += 3 * 4 * 32 * v4;
-  L.taps_off = off;  // [2 buffers][2 ears][tap_stride] int2
-  off += 2 * 2 * 2 * tap_stride;
+  L.taps_off = off;  // [2 buffers][tap_stride] int4 ear pairs
+  off += 2 * 4 * tap_stride;
   L.warp_floats = (off + 31) & ~31;
   off = kWarps * L.warp_floats;
   L.bptr_off = off;
-  off += kMixBMaxBuckets + 4;
+  off += kMixMaxBuckets + 4;
   L.bdir_off = off;
-  off += kMixBMaxBuckets;
+  off += kMixMaxBuckets;
   L.bsrc_off = off;
-  off += kMixWGroupSrcs;
+  off += kMixGroupSrcs;
   L.total_bytes = off * 4;
   return L;
 }
 
 template <int KWIN, int NNZT>
-__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a) {
+__global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) {
   constexpr int COLS = kR + KWIN;
   constexpr int SLICE = 32 * kR + KWIN;
   constexpr int V4 = (SLICE / 4 + 31) / 32;
   constexpr int SLOTS = 3;
   extern __shared__ __align__(128) float smem[];
   __shared__ unsigned s_tbase;
-  const MixWLayout L = mixw_layout(KWIN, a.tap_stride);
+  const MixLayout L = mix_layout(KWIN, a.tap_stride);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* wb = smem + warp * L.warp_floats;
   float* s_slice = wb + L.slice_off;
   float4* s_slot = reinterpret_cast<float4*>(wb + L.slot_off);
-  int2* s_taps = reinterpret_cast<int2*>(wb + L.taps_off);
+  int4* s_taps = reinterpret_cast<int4*>(wb + L.taps_off);  // [2 buffers][tap_stride] ear pairs
   int* s_bptr = reinterpret_cast<int*>(smem + L.bptr_off);
   int* s_bdir = reinterpret_cast<int*>(smem + L.bdir_off);
   int* s_bsrc = reinterpret_cast<int*>(smem + L.bsrc_off);
@@ -831,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a
       for (int i = tid; i < nb; i += kThreads) s_bdir[i] = __ldg(a.bdir + b0 + i);
       gfirst = __ldg(a.bptr + b0);
       const int gn = __ldg(a.bptr + b0 + nb) - gfirst;
-      src_in_smem = gn <= kMixWGroupSrcs;
+      src_in_smem = gn <= kMixGroupSrcs;
       if (src_in_smem)
         for (int i = tid; i < gn; i += kThreads) s_bsrc[i] = __ldg(a.bsrc + gfirst + i);
       __syncthreads();
@@ -854,12 +233,9 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a
         }
       }
       const int dir = s_bdir[k];
-      int2* tb = s_taps + (k & 1) * 2 * a.tap_stride;
-      for (int i = lane; i < a.tap_stride; i += 32) {  // 2 taps (16 B) per copy
-        const int e = i >= a.tap_stride / 2, kk = 2 * (i - e * (a.tap_stride / 2));
-        const int ee = e < a.ears ? e : 0;
-        cp_async16(tb + e * a.tap_stride + kk, a.taps + ((long long)ee * a.dirs + dir) * a.tap_stride + kk);
-      }
+      int4* tb = s_taps + (k & 1) * a.tap_stride;
+      const int4* tg = a.etaps + (long long)dir * a.tap_stride;
+      for (int i = lane; i < a.tap_stride; i += 32) cp_async16(tb + i, tg + i);
       cp_async_commit();
     };
     float accA[16], accB[16];
@@ -929,8 +305,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a
           if (lane + 32 * q < SLICE / 4) *reinterpret_cast<float4*>(sb + 144 * q) = v[q];
       }
       __syncwarp();
-      const int2* tA = s_taps + (k & 1) * 2 * a.tap_stride;
-      const int2* tB = tA + a.tap_stride;
+      const int4* tp = s_taps + (k & 1) * a.tap_stride;
       const int dir = s_bdir[k];
       if (k + 1 < nb) prefetch(k + 1);  // next bucket's loads overlap this bucket's taps
       {
@@ -952,47 +327,44 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a
       const float keepB = a.ears > 1 ? 1.f : 0.f;
       if constexpr (NNZT > 0) {
         float XA0[16], XB0[16], XA1[16], XB1[16];
-        int2 ta = tA[0], tb = tB[0];
-        int2 tan = tA[NNZT > 1 ? 1 : 0], tbn = tB[NNZT > 1 ? 1 : 0];
-        tmem_ld16(XA0, tlane + ta.x);
-        tmem_ld16(XB0, tlane + tb.x);
+        int4 t = tp[0];
+        int4 tn = tp[NNZT > 1 ? 1 : 0];
+        tmem_ld16(XA0, tlane + t.x);
+        tmem_ld16(XB0, tlane + t.z);
 #pragma unroll
         for (int kk = 0; kk < NNZT; ++kk) {
-          const int2 tann = tA[kk + 2 < NNZT ? kk + 2 : NNZT - 1];
-          const int2 tbnn = tB[kk + 2 < NNZT ? kk + 2 : NNZT - 1];
+          const int4 tnn = tp[kk + 2 < NNZT ? kk + 2 : NNZT - 1];
           float(&XA)[16] = (kk & 1) ? XA1 : XA0;
           float(&XB)[16] = (kk & 1) ? XB1 : XB0;
           float(&YA)[16] = (kk & 1) ? XA0 : XA1;
           float(&YB)[16] = (kk & 1) ? XB0 : XB1;
-          const unsigned na = tlane + tan.x, nb2 = tlane + tbn.x;
+          const unsigned na = tlane + tn.x, nb2 = tlane + tn.z;
           tmem_wait_ld();
           if (kk + 1 < NNZT) {
             tmem_ld16(YA, na);
             tmem_ld16(YB, nb2);
           }
-          const float va = __int_as_float(ta.y), vb = __int_as_float(tb.y) * keepB;
+          const float va = __int_as_float(t.y), vb = __int_as_float(t.w) * keepB;
 #pragma unroll
           for (int r = 0; r < 16; r += 2) {
             ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
             ffma2(accB[r], accB[r + 1], XB[r], XB[r + 1], vb);
           }
-          ta = tan;
-          tb = tbn;
-          tan = tann;
-          tbn = tbnn;
+          t = tn;
+          tn = tnn;
         }
       } else {
         const int nA = __ldg(a.row_nnz + dir);
         const int nB = a.ears > 1 ? __ldg(a.row_nnz + a.dirs + dir) : 0;
         const int nk = max(nA, nB);
         for (int kk = 0; kk < nk; ++kk) {
-          const int2 ta = tA[kk], tb = tB[kk];
+          const int4 t = tp[kk];
           float XA[16], XB[16];
-          tmem_ld16(XA, tlane + ta.x);
-          tmem_ld16(XB, tlane + tb.x);
+          tmem_ld16(XA, tlane + t.x);
+          tmem_ld16(XB, tlane + t.z);
           tmem_wait_ld();
-          const float va = kk < nA ? __int_as_float(ta.y) : 0.f;
-          const float vb = kk < nB ? __int_as_float(tb.y) : 0.f;
+          const float va = kk < nA ? __int_as_float(t.y) : 0.f;
+          const float vb = kk < nB ? __int_as_float(t.w) : 0.f;
 #pragma unroll
           for (int r = 0; r < 16; r += 2) {
             ffma2(accA[r], accA[r + 1], XA[r], XA[r + 1], va);
@@ -1026,14 +398,9 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mixw(MixBArgs a
 }
 
 template <int KWIN, int NNZT>
-static cudaError_t launch_mixb_t(const MixBArgs& a, int sm_count, cudaStream_t st) {
-  static const bool warp_private = [] {
-    const char* ev = getenv("TOEP_MIX_KERNEL");
-    return !(ev && ev[0] == 'b');
-  }();
-  const int bytes = warp_private ? mixw_layout(KWIN, a.tap_stride).total_bytes
-                                 : mixb_layout(KWIN, a.tap_stride).total_bytes;
-  auto kern = warp_private ? k_mixw<KWIN, NNZT> : k_mixb<KWIN, NNZT>;
+static cudaError_t launch_mix_t(const MixArgs& a, int sm_count, cudaStream_t st) {
+  const int bytes = mix_layout(KWIN, a.tap_stride).total_bytes;
+  auto kern = k_mix<KWIN, NNZT>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return err;
   long long grid = (long long)sm_count * (512 / (kR + KWIN));  // TMEM-bounded co-residency
@@ -1044,77 +411,23 @@ static cudaError_t launch_mixb_t(const MixBArgs& a, int sm_count, cudaStream_t s
 }
 
 template <int KWIN>
-static cudaError_t mixb_nnz(const MixBArgs& a, int nnz_uniform, int sm, cudaStream_t st) {
+static cudaError_t mix_nnz(const MixArgs& a, int nnz_uniform, int sm, cudaStream_t st) {
   switch (nnz_uniform) {
-    case 8: return launch_mixb_t<KWIN, 8>(a, sm, st);
-    case 16: return launch_mixb_t<KWIN, 16>(a, sm, st);
-    case 24: return launch_mixb_t<KWIN, 24>(a, sm, st);
-    case 32: return launch_mixb_t<KWIN, 32>(a, sm, st);
-    default: return launch_mixb_t<KWIN, 0>(a, sm, st);
+    case 8: return launch_mix_t<KWIN, 8>(a, sm, st);
+    case 16: return launch_mix_t<KWIN, 16>(a, sm, st);
+    case 24: return launch_mix_t<KWIN, 24>(a, sm, st);
+    case 32: return launch_mix_t<KWIN, 32>(a, sm, st);
+    default: return launch_mix_t<KWIN, 0>(a, sm, st);
   }
 }
 
-cudaError_t launch_mixb(const MixBArgs& a, int kwin, int nnz_uniform, int sm_count, cudaStream_t st) {
+cudaError_t launch_mix(const MixArgs& a, int kwin, int nnz_uniform, int sm_count, cudaStream_t st) {
   switch (kwin) {
-    case 112: return mixb_nnz<112>(a, nnz_uniform, sm_count, st);
-    case 240: return mixb_nnz<240>(a, nnz_uniform, sm_count, st);
-    case 496: return mixb_nnz<496>(a, nnz_uniform, sm_count, st);
+    case 112: return mix_nnz<112>(a, nnz_uniform, sm_count, st);
+    case 240: return mix_nnz<240>(a, nnz_uniform, sm_count, st);
+    case 496: return mix_nnz<496>(a, nnz_uniform, sm_count, st);
   }
   return cudaErrorInvalidValue;
-}
-
-// ------------------------------------------------ same-direction source sums ----
-// yb[b][t] = sum over the sources of bucket b (all at one direction) of y_s[t].
-// Pure streaming pass (HBM-bound): float4 loads, up to 4 sources in flight.
-__global__ void __launch_bounds__(256) k_bucket_sum(const float* __restrict__ y, long long y_pitch, long long T,
-                                                    const int* __restrict__ bsrc, const int* __restrict__ bptr,
-                                                    float* __restrict__ yb, long long yb_pitch) {
-  const int b = blockIdx.y;
-  const int i0 = bptr[b], i1 = bptr[b + 1];
-  float* out = yb + (long long)b * yb_pitch;
-  const long long n4 = T >> 2;
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (long long)gridDim.x * blockDim.x) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int i = i0;
-    for (; i + 4 <= i1; i += 4) {
-      float4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(y + (long long)bsrc[i + u] * y_pitch) + q);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc.x += v[u].x;
-        acc.y += v[u].y;
-        acc.z += v[u].z;
-        acc.w += v[u].w;
-      }
-    }
-    for (; i < i1; ++i) {
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(y + (long long)bsrc[i] * y_pitch) + q);
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
-    }
-    reinterpret_cast<float4*>(out)[q] = acc;
-  }
-  if (blockIdx.x == 0) {
-    for (long long t = 4 * n4 + threadIdx.x; t < T; t += blockDim.x) {
-      float acc = 0.f;
-      for (int i = i0; i < i1; ++i) acc += y[(long long)bsrc[i] * y_pitch + t];
-      out[t] = acc;
-    }
-  }
-}
-
-cudaError_t launch_bucket_sum(const float* y, long long y_pitch, long long T, const int* bsrc, const int* bptr,
-                              int buckets, float* yb, long long yb_pitch, int sm_count, cudaStream_t st) {
-  const long long n4 = T >> 2;
-  long long bx = (n4 + 255) / 256;
-  const long long cap = std::max(1LL, (long long)sm_count * 8 / std::max(1, buckets) + 1);
-  if (bx > cap * 64) bx = cap * 64;
-  if (bx < 1) bx = 1;
-  k_bucket_sum<<<dim3((unsigned)bx, (unsigned)buckets), 256, 0, st>>>(y, y_pitch, T, bsrc, bptr, yb, yb_pitch);
-  return cudaGetLastError();
 }
 
 __global__ void k_mix_reduce(const float* __restrict__ part, int groups, int ears, long long part_pitch,

@@ -86,33 +86,9 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st);
 
 // Source -> per-ear partial mix, reflection filters first (g-first order):
 //   part[grp][e][t] = sum_{s in grp} sum_k v_{e,d(s),k} * y_s[t - o_{e,d(s),k}]
-struct MixArgs {
-  const float* y;        // sources, row s at y + s * y_pitch, length T
-  long long T;
-  long long y_pitch;
-  const int* src_dir;    // [S] direction of each source
-  const int4* steps;     // [S] direction-sorted {src, dir, first-of-dir, last-of-dir} per group position
-  int S;
-  const int2* taps;      // same tables as RenderArgs (col = KWIN - o); tap_stride even
-  const int* row_nnz;
-  int tap_stride;
-  int uniform_nnz;
-  int tap_stride_nnz;    // taps per row when uniform_nnz
-  int dirs;
-  int ears;
-  int src_per_group;
-  int groups;
-  int n_tiles;           // ceil(zlen / 2048)
-  long long n_items;     // groups * n_tiles
-  float* part;           // [groups][ears][part_pitch]
-  long long part_pitch;
-  long long zlen;        // T + K - 1
-};
-cudaError_t launch_mix(const MixArgs& a, int kwin, int sm_count, cudaStream_t st);
-
 // Bucketed mix (one pass over the sources): buckets are the sets of sources
 // sharing a direction; item = (bucket group, 2048-sample tile).
-struct MixBArgs {
+struct MixArgs {
   const float* y;        // sources, row s at y + s * y_pitch, length T
   long long T;
   long long y_pitch;
@@ -125,6 +101,7 @@ struct MixBArgs {
   int n_tiles;           // ceil(zlen / 2048)
   long long n_items;     // groups * n_tiles
   const int2* taps;      // ear-major [ears * dirs][tap_stride], col = KWIN - o
+  const int4* etaps;     // [dirs][tap_stride] {col_e0, v_e0, col_e1, v_e1} (k_ear_pair_taps)
   const int* row_nnz;
   int tap_stride;
   int dirs;
@@ -134,11 +111,9 @@ struct MixBArgs {
   long long zlen;        // T + K - 1
   int* nonfinite;        // set to 1 when a non-finite source sample is read (may be null)
 };
-cudaError_t launch_mixb(const MixBArgs& a, int kwin, int nnz_uniform, int sm_count, cudaStream_t st);
-
-// yb[b] = sum of the sources bsrc[bptr[b] .. bptr[b+1]) (all of one direction).
-cudaError_t launch_bucket_sum(const float* y, long long y_pitch, long long T, const int* bsrc, const int* bptr,
-                              int buckets, float* yb, long long yb_pitch, int sm_count, cudaStream_t st);
+cudaError_t launch_mix(const MixArgs& a, int kwin, int nnz_uniform, int sm_count, cudaStream_t st);
+cudaError_t launch_ear_pair_taps(const int2* rows, int dirs, int ears, int stride, int kwin, int4* out,
+                                 cudaStream_t st);
 
 // z[e][t] = sum_g part[g][e][t]  (fixed order, fp32)
 cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long part_pitch, long long zlen,

@@ -462,6 +462,26 @@ __global__ void k_pair_taps(const int2* __restrict__ rows, const int* __restrict
   }
 }
 
+// Ear-interleaved taps for the mixdown: out[d][k] = {col_e0, v_e0, col_e1, v_e1}
+// of rows d and dirs + d (a zero tap at column kwin when there is one ear).
+__global__ void k_ear_pair_taps(const int2* __restrict__ rows, int dirs, int ears, int stride, int kwin,
+                                int4* __restrict__ out) {
+  const long long total = (long long)dirs * stride;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int2 A = rows[i];
+    const int2 B = ears > 1 ? rows[(long long)dirs * stride + i] : make_int2(kwin, 0);
+    out[i] = make_int4(A.x, A.y, B.x, B.y);
+  }
+}
+
+cudaError_t launch_ear_pair_taps(const int2* rows, int dirs, int ears, int stride, int kwin, int4* out,
+                                 cudaStream_t st) {
+  const long long total = (long long)dirs * stride;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+  k_ear_pair_taps<<<std::max(blocks, 1), 256, 0, st>>>(rows, dirs, ears, stride, kwin, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pair_taps(const int2* rows, const int* nnz, int n_seg, int seg, int stride, int kwin, int4* out,
                              int4* out_nnz, cudaStream_t st) {
   const long long total = (long long)n_seg * ((seg + 1) / 2) * stride;

@@ -1,4 +1,4 @@
-"""GPU: the one-pass bucketed mixdown (k_mixb) at its edges, and the fused
+"""GPU: the one-pass bucketed mixdown (k_mix) at its edges, and the fused
 non-finite input check (the reference's DataError for inf/NaN samples,
 engine/__init__.py:162-165) on the render, mix and streaming paths."""
 import numpy as np

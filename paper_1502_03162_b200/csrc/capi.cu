@@ -327,7 +327,15 @@ struct toep_renderer {
   int4* d_pnnz = nullptr;    // [ears][pairs_per_ear]
   int* d_nonfinite = nullptr;  // sticky flag: a kernel read a non-finite input sample
   int4* d_epairs = nullptr;    // [dirs][tap_stride] ear-interleaved taps (mixdown)
+  void* d_gmma = nullptr;      // tensor-core operand tables (render_mma.cu), null if unsupported
+  float* d_gscale = nullptr;   // [ears][dirs_pad]
 };
+
+// TOEP_RENDER_MMA=0 selects the FFMA/TMEM-window kernel for every render (A/B runs)
+static bool render_mma_enabled() {
+  const char* ev = getenv("TOEP_RENDER_MMA");
+  return !(ev && atoi(ev) == 0);
+}
 
 extern "C" {
 
@@ -366,6 +374,14 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
     if (e == cudaSuccess && ears <= 2) e = cudaMalloc(&r->d_epairs, (size_t)dirs * g->tap_stride * sizeof(int4));
     if (e == cudaSuccess && ears <= 2)
       e = launch_ear_pair_taps(g->d_kw, dirs, ears, g->tap_stride, g->kwin, r->d_epairs, nullptr);
+    if (e == cudaSuccess && render_mma_supported(g->length, r->lf_pad)) {
+      const int nch = (dirs + 63) / 64;
+      e = cudaMalloc(&r->d_gmma, render_mma_gbytes(ears, dirs, g->length));
+      if (e == cudaSuccess) e = cudaMalloc(&r->d_gscale, (size_t)ears * nch * 64 * sizeof(float));
+      if (e == cudaSuccess)
+        e = build_render_mma_tables(g->d_raw, g->d_nnz, dirs, ears, g->tap_stride, g->length, r->d_gmma,
+                                    r->d_gscale, nullptr);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
@@ -381,6 +397,8 @@ int toep_renderer_destroy(toep_renderer* r) {
   if (r->d_f) cudaFree(r->d_f);
   if (r->d_nonfinite) cudaFree(r->d_nonfinite);
   if (r->d_epairs) cudaFree(r->d_epairs);
+  if (r->d_gmma) cudaFree(r->d_gmma);
+  if (r->d_gscale) cudaFree(r->d_gscale);
   if (r->d_pairs) cudaFree(r->d_pairs);
   if (r->d_pnnz) cudaFree(r->d_pnnz);
   delete r;
@@ -419,6 +437,30 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
   if (rows > 1 && out_pitch < out_len) return fail(TOEP_ERR_INVALID, "output pitch %lld < %lld", (long long)out_pitch, out_len);
   cudaStream_t st = S(stream);
   const toep_taps* g = r->g;
+  if (r->d_gmma && render_mma_enabled()) {
+    RenderMmaArgs a{};
+    a.x = y;
+    a.nx = ny;
+    a.f = r->d_f;
+    a.lf_pad = r->lf_pad;
+    a.g = r->d_gmma;
+    a.gscale = r->d_gscale;
+    a.kpad = render_mma_kpad(g->length);
+    a.tt = render_mma_tt(a.kpad);
+    a.nchunks = (r->dirs + 63) / 64;
+    a.dirs = r->dirs;
+    a.dirs_pad = a.nchunks * 64;
+    a.ears = r->ears;
+    a.n_titems = (int)((out_len + 128LL * a.tt - 1) / (128LL * a.tt));
+    a.n_units = (long long)a.ears * a.n_titems * a.nchunks;
+    a.out = out;
+    a.out_pitch = out_pitch;
+    a.out_len = out_len;
+    a.nonfinite = r->d_nonfinite;
+    cudaError_t e = launch_render_mma(a, sm_count_cached(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_render_mma");
+    return TOEP_OK;
+  }
   if (g->kwin > 0) {
     if (!aligned16(out) || (rows > 1 && out_pitch % 4 != 0))
       return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");

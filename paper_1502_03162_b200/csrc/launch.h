@@ -37,6 +37,34 @@ struct RenderArgs {
   int* nonfinite;        // set to 1 when a non-finite input sample is read (may be null)
 };
 
+// Tensor-core renderer (render_mma.cu): stage 2 as a split-fp16 GEMM per
+// (ear, 128*tt-output item, 64-direction chunk) unit.
+struct RenderMmaArgs {
+  const float* x;        // source y[nx]
+  long long nx;
+  const float* f;        // [ears][lf_pad] resonance taps, zero padded
+  int lf_pad;
+  const void* g;         // [ears][nchunks][hi, lo][canonical 64 x kpad] fp16 (build_render_mma_tables)
+  const float* gscale;   // [ears][dirs_pad] per-direction unscale 2^-q
+  int kpad;              // round_up(K, 16)
+  int tt;                // 128-output tiles per item (2 when kpad <= 128)
+  int nchunks;           // ceil(dirs / 64)
+  int dirs, dirs_pad, ears;
+  int n_titems;          // ceil(out_len / (128 * tt))
+  long long n_units;     // ears * n_titems * nchunks
+  float* out;            // row (e * dirs + d) at out + row * out_pitch
+  long long out_pitch;
+  long long out_len;
+  int* nonfinite;
+};
+bool render_mma_supported(int K, int lf_pad);
+int render_mma_kpad(int K);
+int render_mma_tt(int kpad);
+size_t render_mma_gbytes(int ears, int dirs, int K);
+cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, int ears, int stride, int K,
+                                    void* g, float* gscale, cudaStream_t st);
+cudaError_t launch_render_mma(const RenderMmaArgs& a, int sm_count, cudaStream_t st);
+
 // TMA tensor maps over the output rows ([rows][out_len], row stride out_pitch):
 // box {256, 2} for direction pairs and {256, 1} for a trailing odd direction.
 struct RenderMaps {

@@ -438,6 +438,8 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
   cudaStream_t st = S(stream);
   const toep_taps* g = r->g;
   if (r->d_gmma && render_mma_enabled()) {
+    if (!aligned16(out) || (rows > 1 && out_pitch % 4 != 0))
+      return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");
     RenderMmaArgs a{};
     a.x = y;
     a.nx = ny;
@@ -457,7 +459,10 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.out_pitch = out_pitch;
     a.out_len = out_len;
     a.nonfinite = r->d_nonfinite;
-    cudaError_t e = launch_render_mma(a, sm_count_cached(), st);
+    CUtensorMap map;
+    cudaError_t e = make_render_mma_map(out, r->ears, r->dirs, out_len, rows > 1 ? out_pitch : round_up(out_len, 4), &map);
+    if (e != cudaSuccess) return cuda_fail(e, "tensor map (output rows)");
+    e = launch_render_mma(a, map, sm_count_cached(), st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_render_mma");
     return TOEP_OK;
   }

@@ -63,7 +63,9 @@ int render_mma_tt(int kpad);
 size_t render_mma_gbytes(int ears, int dirs, int K);
 cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, int ears, int stride, int K,
                                     void* g, float* gscale, cudaStream_t st);
-cudaError_t launch_render_mma(const RenderMmaArgs& a, int sm_count, cudaStream_t st);
+cudaError_t make_render_mma_map(float* out, int ears, int dirs, long long out_len, long long out_pitch,
+                                CUtensorMap* m);
+cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st);
 
 // TMA tensor maps over the output rows ([rows][out_len], row stride out_pitch):
 // box {256, 2} for direction pairs and {256, 1} for a trailing odd direction.

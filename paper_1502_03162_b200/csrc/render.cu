@@ -563,6 +563,23 @@ cudaError_t make_render_maps(float* out, long long rows, long long out_len, long
   return cudaSuccess;
 }
 
+// 3-D map over the rendered rows for the tensor-core kernel: dims {out_len,
+// dirs, ears}, box {32 t, 32 directions, 1}; rows past `dirs` (the padding of
+// the last 64-direction chunk) and samples past out_len are clipped by TMA.
+cudaError_t make_render_mma_map(float* out, int ears, int dirs, long long out_len, long long out_pitch,
+                                CUtensorMap* m) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) || (out_pitch * 4) % 16) return cudaErrorInvalidValue;
+  const cuuint64_t dims[3] = {(cuuint64_t)out_len, (cuuint64_t)dirs, (cuuint64_t)ears};
+  const cuuint64_t strides[2] = {(cuuint64_t)out_pitch * 4, (cuuint64_t)out_pitch * 4 * dirs};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 int render_kwin_for(int K) {
   if (K <= 113) return 112;
   if (K <= 241) return 240;

@@ -37,6 +37,22 @@
 
 namespace toep {
 
+#ifndef TOEP_MMA_NOMMA
+#define TOEP_MMA_NOMMA 0
+#endif
+#ifndef TOEP_MMA_PROF
+#define TOEP_MMA_PROF 0
+#endif
+#if TOEP_MMA_PROF
+#define PW(slot, ...)                \
+  do {                               \
+    const long long _t0 = clock64(); \
+    __VA_ARGS__;                     \
+    prof[slot] += clock64() - _t0;   \
+  } while (0)
+#else
+#define PW(slot, ...) __VA_ARGS__
+#endif
 constexpr int kMmaM = 128;        // outputs per t-tile
 constexpr int kMmaN = 64;         // directions per chunk
 constexpr int kMmaBuilderWarps = 6;
@@ -130,6 +146,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
   __shared__ unsigned s_tbase;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if TOEP_MMA_PROF
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+#endif
   if (warp == 0) tmem_alloc<256>(&s_tbase);
   if (tid == 32) {
     mbar_init(a_full, 1);
@@ -162,7 +182,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
       for (long long u = u0; u < u1; ++u) {
         const int c = (int)(u % nch);
         const int e = (int)(u / nch / a.n_titems);
-        mbar_wait(&b_empty[bs], bph ^ 1u);
+        PW(0, mbar_wait_sleep(&b_empty[bs], bph ^ 1u));
         mbar_arrive_expect_tx(&b_full[bs], (unsigned)b_chunk_bytes);
         bulk_load(sB + bs * b_chunk_bytes, g + ((long long)e * nch + c) * b_chunk_bytes, (unsigned)b_chunk_bytes,
                   &b_full[bs]);
@@ -184,12 +204,12 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
         const long long item = u / nch;
         if (item != cur) {
           if (cur >= 0) mma_commit(a_empty);  // A of the previous item is free once its MMAs retire
-          mbar_wait(a_full, a_ph);
+          PW(1, mbar_wait_sleep(a_full, a_ph));
           a_ph ^= 1u;
           cur = item;
         }
-        mbar_wait(&b_full[bs], bph);
-        mbar_wait(&acc_empty[as], aph ^ 1u);
+        PW(2, mbar_wait_sleep(&b_full[bs], bph));
+        PW(3, mbar_wait_sleep(&acc_empty[as], aph ^ 1u));
         tmem_fence_after();
         for (int tt = 0; tt < TT; ++tt) {
           const unsigned d = tbase + (unsigned)(as * TT * kMmaN + tt * kMmaN);
@@ -199,7 +219,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
             const unsigned pa = sa + (unsigned)((tt * 2 + (p == 2 ? 1 : 0)) * a_part_bytes);
             const unsigned pb = sb + (unsigned)(bs * b_chunk_bytes + (p == 1 ? 1 : 0) * b_part_bytes);
             for (int ks = 0; ks < KS; ++ks) {
+#if !TOEP_MMA_NOMMA
               mma_f16(d, mma_sdesc(pa + ks * kMmaM * 32), mma_sdesc(pb + ks * kMmaN * 32), idesc, acc);
+#endif
               acc = 1;
             }
           }
@@ -232,7 +254,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
       const int ti = (int)(item % a.n_titems), e = (int)(item / a.n_titems);
       const long long T0 = (long long)ti * kMmaM * TT;
       const long long y0 = T0 - (KP - 1) - (a.lf_pad - 1);
-      mbar_wait(a_empty, a_ph ^ 1u);  // MMAs of the previous item retired (first pass: free)
+      PW(4, mbar_wait_sleep(a_empty, a_ph ^ 1u));  // MMAs of the previous item retired (first pass: free)
       a_ph ^= 1u;
       if (e != cur_e)
         for (int i = bt; i < a.lf_pad; i += kMmaBuilders) s_f[i] = a.f[(long long)e * a.lf_pad + i];
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
       const int sexp = mx > 0.f ? 13 - ilogbf(mx) : 0;  // max |yf| * 2^sexp in [2^13, 2^14)
       const float scale = ldexpf(1.f, sexp);
       if (bt == 0) {
-        mbar_wait(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1));
+        mbar_wait_sleep(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1));
         s_sc[nitem & 1] = ldexpf(1.f, -sexp);
         mbar_arrive(&sc_full[nitem & 1]);
       }
@@ -311,11 +333,11 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
           if (lane == 0) mbar_arrive(&sc_empty[nitem & 1]);
         }
         ++nitem;
-        mbar_wait(&sc_full[nitem & 1], (unsigned)((nitem >> 1) & 1));
+        mbar_wait_sleep(&sc_full[nitem & 1], (unsigned)((nitem >> 1) & 1));
         unscale = s_sc[nitem & 1];
         cur = item;
       }
-      mbar_wait(&acc_full[as], aph);
+      PW(5, mbar_wait_sleep(&acc_full[as], aph));
       tmem_fence_after();
       const long long T0 = (long long)ti * kMmaM * TT;
       const int d0 = c * kMmaN;

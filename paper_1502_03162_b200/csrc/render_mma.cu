@@ -19,7 +19,7 @@
 // for g -- and unscaled exactly in the epilogue, so the split never meets
 // fp16 under/overflow.  Measured rel. L2 ~6e-7 (tools/microbench/mma_probe.cu).
 //
-// Persistent, warp-specialised CTA (one per SM, 12 warps):
+// Persistent, warp-specialised CTA (one per SM, 16 warps):
 //   warp 0      : TMA producer -- G chunks (pre-laid-out canonical fp16 hi/lo,
 //                 32 KB for KPAD 128) into a 2-deep ring (cp.async.bulk + mbarrier)
 //   warp 1      : MMA issuer (one elected lane): per chunk 3 x KPAD/16
@@ -27,8 +27,10 @@
 //   warps 2-7   : A builders -- stage 1 (resonance FIR) for the item's yf tile,
 //                 the per-tile scale, and the Hankel A tile in the canonical
 //                 K-major layout (hi and lo), once per item (TT x 128 outputs)
-//   warps 8-11  : epilogue -- tcgen05.ld the accumulator (lane = output t),
-//                 unscale, coalesced stores (32 consecutive t per instruction)
+//   warps 8-15  : epilogue -- tcgen05.ld the accumulator (lane = output t; two
+//                 warps per lane quarter, 32 columns each), unscale, stage a
+//                 [32 directions][32 t] block in shared memory, TMA tensor store
+//                 (3-D map {t, direction, ear} clips the padding directions)
 #include <algorithm>
 #include <cuda_fp16.h>
 
@@ -56,7 +58,7 @@ namespace toep {
 constexpr int kMmaM = 128;        // outputs per t-tile
 constexpr int kMmaN = 64;         // directions per chunk
 constexpr int kMmaBuilderWarps = 6;
-constexpr int kMmaEpiWarps = 4;
+constexpr int kMmaEpiWarps = 8;  // two per TMEM lane quarter (32 columns each)
 constexpr int kMmaWarps = 2 + kMmaBuilderWarps + kMmaEpiWarps;
 constexpr int kMmaThreads = 32 * kMmaWarps;
 constexpr int kMmaBuilders = 32 * kMmaBuilderWarps;
@@ -93,7 +95,7 @@ __device__ __forceinline__ unsigned pack_half2(__half a, __half b) {
 }
 
 struct MmaSmem {
-  int a_off, b_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total;
+  int a_off, b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total;
 };
 
 __host__ __device__ inline MmaSmem mma_smem(int kpad, int tt, int lf_pad) {
@@ -103,6 +105,8 @@ __host__ __device__ inline MmaSmem mma_smem(int kpad, int tt, int lf_pad) {
   L.a_off = 0;
   L.b_off = a_bytes;
   int off = a_bytes + b_bytes;  // floats from here (all offsets in bytes)
+  L.st_off = off;               // epilogue staging: [epilogue warps][32 directions][32 t]
+  off += kMmaEpiWarps * 32 * 32 * 4;
   L.y_off = off;
   off += ((kMmaM * tt + kpad + lf_pad + 31) & ~31) * 4;
   L.yf_off = off;
@@ -119,7 +123,14 @@ __host__ __device__ inline MmaSmem mma_smem(int kpad, int tt, int lf_pad) {
   return L;
 }
 
-__global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) {
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const float* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tm),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kMmaThreads, 1)
+    k_render_mma(RenderMmaArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   const int TT = a.tt, KP = a.kpad, KS = KP / 16;
@@ -316,7 +327,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
     if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
   } else {
     // ===== epilogue: TMEM -> registers -> HBM =====
-    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int q = warp & 3;                                   // TMEM lane quarter of this warp
+    const int half = (warp - 2 - kMmaBuilderWarps) >> 2;      // which 32 of the chunk's 64 columns
+    float* stg = reinterpret_cast<float*>(sm + L.st_off) + (warp - 2 - kMmaBuilderWarps) * 32 * 32;
     const unsigned tq = tbase + ((unsigned)(32 * q) << 16);
     int as = 0;
     unsigned aph = 0;
@@ -340,24 +353,28 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
       PW(5, mbar_wait_sleep(&acc_full[as], aph));
       tmem_fence_after();
       const long long T0 = (long long)ti * kMmaM * TT;
-      const int d0 = c * kMmaN;
-      const int nd = min(kMmaN, a.dirs - d0);  // directions of this chunk that exist
-      const float* gs = a.gscale + (long long)e * a.dirs_pad + d0;
+      const int d0 = c * kMmaN + 32 * half;  // this warp's 32 directions of the chunk
+      // per-direction unscale for the warp's 32 columns: lane j holds column j's factor
+      const float gsl = (d0 + lane < a.dirs ? __ldg(a.gscale + (long long)e * a.dirs_pad + d0 + lane) : 0.f) * unscale;
 #pragma unroll 1
       for (int tt = 0; tt < TT; ++tt) {
-        const long long t = T0 + kMmaM * tt + 32 * q + lane;
-        float* p = a.out + ((long long)e * a.dirs + d0) * a.out_pitch + t;
-        const bool tok = t < a.out_len;
-#pragma unroll 1
-        for (int cb = 0; cb < kMmaN; cb += 16) {
+        const long long t0 = T0 + kMmaM * tt + 32 * q;
+        if (t0 >= a.out_len) continue;
+        if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging block
+        __syncwarp();
+#pragma unroll
+        for (int cb = 0; cb < 32; cb += 16) {
           float v[16];
-          tmem_ld16(v, tq + (unsigned)(as * TT * kMmaN + tt * kMmaN + cb));
+          tmem_ld16(v, tq + (unsigned)(as * TT * kMmaN + tt * kMmaN + 32 * half + cb));
           tmem_wait_ld();
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            if (tok && cb + jj < nd) *p = v[jj] * (unscale * __ldg(gs + cb + jj));
-            p += a.out_pitch;
-          }
+          for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * __shfl_sync(0xffffffffu, gsl, cb + jj);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (elect_one()) {
+          tma_store_3d(&tm, stg, (int)t0, d0, e);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
       tmem_fence_before();
@@ -369,6 +386,12 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_render_mma(RenderMmaArgs a) 
       }
     }
   }
+  if (warp >= 2 + kMmaBuilderWarps && lane == 0) bulk_wait_all();
+#if TOEP_MMA_PROF
+  if (blockIdx.x == 7 && lane == 0 && (warp <= 2 || warp == 8))
+    printf("prof cta7 warp %d total %lld: b_empty %lld a_full %lld b_full %lld acc_empty %lld a_empty %lld acc_full %lld\n",
+           warp, clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
+#endif
   tmem_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<256>(tbase);
@@ -432,13 +455,13 @@ cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_render_mma(const RenderMmaArgs& a, int sm_count, cudaStream_t st) {
+cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st) {
   const MmaSmem L = mma_smem(a.kpad, a.tt, a.lf_pad);
   cudaError_t err = cudaFuncSetAttribute(k_render_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
   long long grid = std::min<long long>(sm_count, a.n_units);
   if (grid < 1) return cudaSuccess;
-  k_render_mma<<<(unsigned)grid, kMmaThreads, L.total, st>>>(a);
+  k_render_mma<<<(unsigned)grid, kMmaThreads, L.total, st>>>(a, map);
   return cudaGetLastError();
 }
 

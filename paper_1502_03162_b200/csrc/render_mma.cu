@@ -32,6 +32,7 @@
 //                 [32 directions][32 t] block in shared memory, TMA tensor store
 //                 (3-D map {t, direction, ear} clips the padding directions)
 #include <algorithm>
+#include <cstdio>
 #include <cuda_fp16.h>
 
 #include "common.cuh"

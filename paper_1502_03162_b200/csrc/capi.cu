@@ -375,9 +375,9 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
     if (e == cudaSuccess && ears <= 2)
       e = launch_ear_pair_taps(g->d_kw, dirs, ears, g->tap_stride, g->kwin, r->d_epairs, nullptr);
     if (e == cudaSuccess && render_mma_supported(g->length, r->lf_pad)) {
-      const int nch = (dirs + 63) / 64;
+      const int cn = render_mma_chunk(), nch = (dirs + cn - 1) / cn;
       e = cudaMalloc(&r->d_gmma, render_mma_gbytes(ears, dirs, g->length));
-      if (e == cudaSuccess) e = cudaMalloc(&r->d_gscale, (size_t)ears * nch * 64 * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&r->d_gscale, (size_t)ears * nch * cn * sizeof(float));
       if (e == cudaSuccess)
         e = build_render_mma_tables(g->d_raw, g->d_nnz, dirs, ears, g->tap_stride, g->length, r->d_gmma,
                                     r->d_gscale, nullptr);
@@ -449,9 +449,9 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.gscale = r->d_gscale;
     a.kpad = render_mma_kpad(g->length);
     a.tt = render_mma_tt(a.kpad);
-    a.nchunks = (r->dirs + 63) / 64;
+    a.nchunks = (r->dirs + render_mma_chunk() - 1) / render_mma_chunk();
     a.dirs = r->dirs;
-    a.dirs_pad = a.nchunks * 64;
+    a.dirs_pad = a.nchunks * render_mma_chunk();
     a.ears = r->ears;
     a.n_titems = (int)((out_len + 128LL * a.tt - 1) / (128LL * a.tt));
     a.n_units = (long long)a.ears * a.n_titems * a.nchunks;

@@ -44,11 +44,11 @@ struct RenderMmaArgs {
   long long nx;
   const float* f;        // [ears][lf_pad] resonance taps, zero padded
   int lf_pad;
-  const void* g;         // [ears][nchunks][hi, lo][canonical 64 x kpad] fp16 (build_render_mma_tables)
+  const void* g;         // [ears][nchunks][hi, lo][canonical chunk x kpad] fp16 (build_render_mma_tables)
   const float* gscale;   // [ears][dirs_pad] per-direction unscale 2^-q
   int kpad;              // round_up(K, 16)
-  int tt;                // 128-output tiles per item (2 when kpad <= 128)
-  int nchunks;           // ceil(dirs / 64)
+  int tt;                // 128-output tiles per item (1)
+  int nchunks;           // ceil(dirs / render_mma_chunk())
   int dirs, dirs_pad, ears;
   int n_titems;          // ceil(out_len / (128 * tt))
   long long n_units;     // ears * n_titems * nchunks
@@ -60,6 +60,7 @@ struct RenderMmaArgs {
 bool render_mma_supported(int K, int lf_pad);
 int render_mma_kpad(int K);
 int render_mma_tt(int kpad);
+int render_mma_chunk();  // directions per G chunk (MMA N)
 size_t render_mma_gbytes(int ears, int dirs, int K);
 cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, int ears, int stride, int K,
                                     void* g, float* gscale, cudaStream_t st);

@@ -19,15 +19,21 @@
 // for g -- and unscaled exactly in the epilogue, so the split never meets
 // fp16 under/overflow.  Measured rel. L2 ~6e-7 (tools/microbench/mma_probe.cu).
 //
-// Persistent, warp-specialised CTA (one per SM, 16 warps):
+// The Hankel operand A lives in TMEM (lane t = output t, column j = the fp16
+// pair {A[t][2j], A[t][2j+1]}), so each MMA reads only G from shared memory:
+// with A in shared memory the N = 64 MMAs were shared-memory-bandwidth bound
+// (A re-read per direction chunk).
+//
+// Persistent, warp-specialised CTA (one per SM, 18 warps):
 //   warp 0      : TMA producer -- G chunks (pre-laid-out canonical fp16 hi/lo,
-//                 32 KB for KPAD 128) into a 2-deep ring (cp.async.bulk + mbarrier)
-//   warp 1      : MMA issuer (one elected lane): per chunk 3 x KPAD/16
-//                 tcgen05.mma per t-tile into a double-buffered TMEM accumulator
-//   warps 2-7   : A builders -- stage 1 (resonance FIR) for the item's yf tile,
-//                 the per-tile scale, and the Hankel A tile in the canonical
-//                 K-major layout (hi and lo), once per item (TT x 128 outputs)
-//   warps 8-15  : epilogue -- tcgen05.ld the accumulator (lane = output t; two
+//                 28 KB for KPAD 112) into a kMmaBStages-deep ring
+//   warp 1      : MMA issuer (one elected lane): per chunk and t-tile,
+//                 3 x KPAD/16 tcgen05.mma (A from TMEM, G from shared memory)
+//                 into a double-buffered TMEM accumulator
+//   warps 2-9   : A builders -- stage 1 (resonance FIR) for the item's yf tile,
+//                 the per-tile scale, then every thread writes its TMEM lane's
+//                 Hankel row (hi and lo) with tcgen05.st; once per item
+//   warps 10-17 : epilogue -- tcgen05.ld the accumulator (lane = output t; two
 //                 warps per lane quarter, 32 columns each), unscale, stage a
 //                 [32 directions][32 t] block in shared memory, TMA tensor store
 //                 (3-D map {t, direction, ear} clips the padding directions)
@@ -57,12 +63,18 @@ namespace toep {
 #define PW(slot, ...) __VA_ARGS__
 #endif
 constexpr int kMmaM = 128;        // outputs per t-tile
-constexpr int kMmaN = 64;         // directions per chunk
-constexpr int kMmaBuilderWarps = 6;
-constexpr int kMmaEpiWarps = 8;  // two per TMEM lane quarter (32 columns each)
+constexpr int kMmaN = 128;        // directions per chunk (M = 128, N = 128: full tensor rate, N = 64 runs at half)
+constexpr int kMmaBuilderWarps = 8;  // two per TMEM lane quarter
+constexpr int kMmaEpiWarps = 8;      // two per TMEM lane quarter (64 columns each)
 constexpr int kMmaWarps = 2 + kMmaBuilderWarps + kMmaEpiWarps;
 constexpr int kMmaThreads = 32 * kMmaWarps;
 constexpr int kMmaBuilders = 32 * kMmaBuilderWarps;
+constexpr int kMmaBStages = 2;
+#ifndef TOEP_MMA_CLUSTER
+#define TOEP_MMA_CLUSTER 4
+#endif
+constexpr int kMmaCluster = TOEP_MMA_CLUSTER;  // CTAs sharing each G chunk load (TMA multicast)
+constexpr int kMmaAccCols = 2 * kMmaN;  // accumulators: 2 buffers x 128 columns; A buffers follow
 
 // byte offset of element (r, k) in an R-row, K-major, SWIZZLE_NONE canonical
 // operand: 8x16-byte core matrices, rows of a core at 16 B, the two K halves
@@ -76,16 +88,54 @@ __device__ __forceinline__ uint64_t mma_sdesc(unsigned saddr) {
          ((uint64_t)1 << 46);  // version 1 (sm_100), base offset 0, SWIZZLE_NONE
 }
 
-__device__ __forceinline__ void mma_f16(unsigned d_tmem, uint64_t da, uint64_t db, uint32_t idesc, int accumulate) {
+// D[tmem] (+)= A[tmem] * B[smem]^T, fp16 inputs, fp32 accumulate
+__device__ __forceinline__ void mma_f16_ts(unsigned d_tmem, unsigned a_tmem, uint64_t db, uint32_t idesc,
+                                           int accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned num_clusters_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 1-D bulk copy global -> the same shared-memory offset of every CTA in `mask`,
+// completion counted on each destination CTA's mbarrier at `bar`'s offset
+__device__ __forceinline__ void bulk_load_multicast(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar,
+                                                    unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// MMA completion -> arrive on the barrier at `bar`'s offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_multicast(uint64_t* bar, unsigned short mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                   "r"(smem_u32(bar)),
+               "h"(mask)
                : "memory");
 }
 
@@ -95,33 +145,10 @@ __device__ __forceinline__ unsigned pack_half2(__half a, __half b) {
   return (unsigned)__half_as_ushort(a) | ((unsigned)__half_as_ushort(b) << 16);
 }
 
-struct MmaSmem {
-  int a_off, b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total;
-};
-
-__host__ __device__ inline MmaSmem mma_smem(int kpad, int tt, int lf_pad) {
-  MmaSmem L{};
-  const int a_bytes = tt * 2 * kMmaM * kpad * 2;
-  const int b_bytes = 2 * 2 * kMmaN * kpad * 2;
-  L.a_off = 0;
-  L.b_off = a_bytes;
-  int off = a_bytes + b_bytes;  // floats from here (all offsets in bytes)
-  L.st_off = off;               // epilogue staging: [epilogue warps][32 directions][32 t]
-  off += kMmaEpiWarps * 32 * 32 * 4;
-  L.y_off = off;
-  off += ((kMmaM * tt + kpad + lf_pad + 31) & ~31) * 4;
-  L.yf_off = off;
-  off += ((kMmaM * tt + kpad + 31) & ~31) * 4;
-  L.f_off = off;
-  off += ((lf_pad + 31) & ~31) * 4;
-  L.red_off = off;
-  off += 32 * 4;
-  L.sc_off = off;
-  off += 8 * 4;
-  L.bars_off = off;
-  off += 16 * 8;
-  L.total = off + 1024;  // alignment slack
-  return L;
+__device__ __forceinline__ void tmem_st8(unsigned ta, const unsigned (&w)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
 }
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const float* src, int c0, int c1, int c2) {
@@ -130,31 +157,59 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const float*
                : "memory");
 }
 
+struct MmaSmem {
+  int b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total;
+};
+
+__host__ __device__ inline MmaSmem mma_smem(int kpad, int lf_pad) {
+  MmaSmem L{};
+  L.b_off = 0;  // [kMmaBStages][hi, lo][canonical 128 x kpad] fp16
+  int off = kMmaBStages * 2 * kMmaN * kpad * 2;
+  L.st_off = off;  // epilogue staging: [epilogue warps][2 buffers][32 directions][32 t] fp32
+  off += kMmaEpiWarps * 2 * 32 * 32 * 4;
+  L.y_off = off;
+  off += ((kMmaM + kpad + lf_pad + 31) & ~31) * 4;
+  L.yf_off = off;
+  off += ((kMmaM + kpad + 31) & ~31) * 4;
+  L.f_off = off;
+  off += ((lf_pad + 31) & ~31) * 4;
+  L.red_off = off;
+  off += 32 * 4;
+  L.sc_off = off;
+  off += 8 * 4;
+  L.bars_off = off;
+  off += (12 + 2 * kMmaBStages) * 8;
+  L.total = off + 1024;  // alignment slack
+  return L;
+}
+
+// A buffers in TMEM after the two accumulators: two when they fit (the next
+// item's Hankel rows are written while this item's MMAs run), else one
+__host__ __device__ inline int mma_a_buffers(int kpad) { return kMmaAccCols + 2 * kpad <= 512 ? 2 : 1; }
+
 __global__ void __launch_bounds__(kMmaThreads, 1)
     k_render_mma(RenderMmaArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  const int TT = a.tt, KP = a.kpad, KS = KP / 16;
-  const MmaSmem L = mma_smem(KP, TT, a.lf_pad);
-  const int a_part_bytes = kMmaM * KP * 2;
+  const int KP = a.kpad, KS = KP / 16, NA = mma_a_buffers(KP);
+  const MmaSmem L = mma_smem(KP, a.lf_pad);
   const int b_part_bytes = kMmaN * KP * 2;
   const int b_chunk_bytes = 2 * b_part_bytes;
-  unsigned char* sA = sm + L.a_off;  // [TT][hi, lo][canonical 128 x KP]
-  unsigned char* sB = sm + L.b_off;  // [2 stages][hi, lo][canonical 64 x KP]
+  unsigned char* sB = sm + L.b_off;
   float* s_y = reinterpret_cast<float*>(sm + L.y_off);
   float* s_yf = reinterpret_cast<float*>(sm + L.yf_off);
   float* s_f = reinterpret_cast<float*>(sm + L.f_off);
   float* s_red = reinterpret_cast<float*>(sm + L.red_off);
   float* s_sc = reinterpret_cast<float*>(sm + L.sc_off);  // per item (ring of 2): 2^-s
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars_off);
-  uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 1;
-  uint64_t* b_full = bars + 2;       // [2]
-  uint64_t* b_empty = bars + 4;      // [2]
-  uint64_t* acc_full = bars + 6;     // [2]
-  uint64_t* acc_empty = bars + 8;    // [2]
-  uint64_t* sc_full = bars + 10;     // [2]
-  uint64_t* sc_empty = bars + 12;    // [2]
+  uint64_t* a_full = bars + 0;     // [2]
+  uint64_t* a_empty = bars + 2;    // [2]
+  uint64_t* acc_full = bars + 4;   // [2]
+  uint64_t* acc_empty = bars + 6;  // [2]
+  uint64_t* sc_full = bars + 8;    // [2]
+  uint64_t* sc_empty = bars + 10;  // [2]
+  uint64_t* b_full = bars + 12;    // [kMmaBStages]
+  uint64_t* b_empty = b_full + kMmaBStages;
   __shared__ unsigned s_tbase;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -162,28 +217,40 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
   long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_start = clock64();
 #endif
-  if (warp == 0) tmem_alloc<256>(&s_tbase);
+  if (warp == 0) tmem_alloc<512>(&s_tbase);
   if (tid == 32) {
-    mbar_init(a_full, 1);
-    mbar_init(a_empty, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], 1);
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], kMmaEpiWarps);
       mbar_init(&sc_full[i], 1);
       mbar_init(&sc_empty[i], kMmaEpiWarps);
     }
+    for (int i = 0; i < kMmaBStages; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], kMmaCluster);  // every CTA of the cluster frees the stage
+    }
     mbar_fence_init();
   }
   tmem_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barrier inits visible cluster-wide before any multicast lands
   tmem_fence_after();
   const unsigned tbase = s_tbase;
 
-  const long long u0 = a.n_units * blockIdx.x / gridDim.x;
-  const long long u1 = a.n_units * (blockIdx.x + 1) / gridDim.x;
+  // Work: groups of kMmaCluster consecutive 128-output tiles of one ear; the
+  // cluster walks a contiguous range of groups, CTA `crank` renders tile
+  // 4*group + crank of each, all CTAs stepping through the same G chunks in
+  // lockstep (unit = (group, chunk)).  Tiles past the end render zeros and
+  // store nothing.
   const int nch = a.nchunks;
+  const int crank = (int)cluster_ctarank();
+  const long long gpe = (a.n_titems + kMmaCluster - 1) / kMmaCluster;  // groups per ear
+  const long long ngroups = gpe * a.ears;
+  const long long g0 = ngroups * cluster_id_x() / num_clusters_x();
+  const long long g1 = ngroups * (cluster_id_x() + 1) / num_clusters_x();
+  const long long u0 = g0 * nch, u1 = g1 * nch;
+  const unsigned short cmask = (unsigned short)((1u << kMmaCluster) - 1u);
 
   if (warp == 0) {
     // ===== G chunk producer =====
@@ -193,12 +260,14 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const unsigned char* g = reinterpret_cast<const unsigned char*>(a.g);
       for (long long u = u0; u < u1; ++u) {
         const int c = (int)(u % nch);
-        const int e = (int)(u / nch / a.n_titems);
-        PW(0, mbar_wait_sleep(&b_empty[bs], bph ^ 1u));
+        const int e = (int)(u / nch / gpe);
+        PW(0, mbar_wait_sleep(&b_empty[bs], bph ^ 1u));  // the stage is free in every CTA of the cluster
         mbar_arrive_expect_tx(&b_full[bs], (unsigned)b_chunk_bytes);
-        bulk_load(sB + bs * b_chunk_bytes, g + ((long long)e * nch + c) * b_chunk_bytes, (unsigned)b_chunk_bytes,
-                  &b_full[bs]);
-        if (++bs == 2) {
+        const int slice = b_chunk_bytes / kMmaCluster;  // this CTA loads one slice for the whole cluster
+        bulk_load_multicast(sB + bs * b_chunk_bytes + crank * slice,
+                            g + ((long long)e * nch + c) * b_chunk_bytes + crank * slice, (unsigned)slice,
+                            &b_full[bs], cmask);
+        if (++bs == kMmaBStages) {
           bs = 0;
           bph ^= 1u;
         }
@@ -208,39 +277,39 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     // ===== MMA issuer =====
     if (elect_one()) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(kMmaN >> 3) << 17) | ((uint32_t)(kMmaM >> 4) << 24);
-      int bs = 0, as = 0;
-      unsigned bph = 0, aph = 0, a_ph = 0;
+      int bs = 0, as = 0, ab = -1;
+      unsigned bph = 0, aph = 0, a_ph[2] = {0u, 0u};
       long long cur = -1;
-      const unsigned sa = smem_u32(sA), sb = smem_u32(sB);
+      const unsigned sb = smem_u32(sB);
       for (long long u = u0; u < u1; ++u) {
         const long long item = u / nch;
         if (item != cur) {
-          if (cur >= 0) mma_commit(a_empty);  // A of the previous item is free once its MMAs retire
-          PW(1, mbar_wait_sleep(a_full, a_ph));
-          a_ph ^= 1u;
+          if (ab >= 0) mma_commit(&a_empty[ab]);  // this A buffer is free once its MMAs retire
+          ab = (ab + 1) % NA;
+          PW(1, mbar_wait_sleep(&a_full[ab], a_ph[ab]));
+          a_ph[ab] ^= 1u;
           cur = item;
         }
         PW(2, mbar_wait_sleep(&b_full[bs], bph));
         PW(3, mbar_wait_sleep(&acc_empty[as], aph ^ 1u));
         tmem_fence_after();
-        for (int tt = 0; tt < TT; ++tt) {
-          const unsigned d = tbase + (unsigned)(as * TT * kMmaN + tt * kMmaN);
-          int acc = 0;
+        const unsigned d = tbase + (unsigned)(as * kMmaN);
+        const unsigned at = tbase + (unsigned)(kMmaAccCols + ab * KP);  // [hi | lo] KP/2 columns each
+        int acc = 0;
 #pragma unroll 1
-          for (int p = 0; p < 3; ++p) {  // hi*hi, hi*lo, lo*hi
-            const unsigned pa = sa + (unsigned)((tt * 2 + (p == 2 ? 1 : 0)) * a_part_bytes);
-            const unsigned pb = sb + (unsigned)(bs * b_chunk_bytes + (p == 1 ? 1 : 0) * b_part_bytes);
-            for (int ks = 0; ks < KS; ++ks) {
+        for (int p = 0; p < 3; ++p) {  // hi*hi, hi*lo, lo*hi
+          const unsigned pa = at + (unsigned)(p == 2 ? KP / 2 : 0);
+          const unsigned pb = sb + (unsigned)(bs * b_chunk_bytes + (p == 1 ? 1 : 0) * b_part_bytes);
+          for (int ks = 0; ks < KS; ++ks) {
 #if !TOEP_MMA_NOMMA
-              mma_f16(d, mma_sdesc(pa + ks * kMmaM * 32), mma_sdesc(pb + ks * kMmaN * 32), idesc, acc);
+            mma_f16_ts(d, pa + 8 * ks, mma_sdesc(pb + ks * kMmaN * 32), idesc, acc);
 #endif
-              acc = 1;
-            }
+            acc = 1;
           }
         }
-        mma_commit(&b_empty[bs]);
+        mma_commit_multicast(&b_empty[bs], cmask);
         mma_commit(&acc_full[as]);
-        if (++bs == 2) {
+        if (++bs == kMmaBStages) {
           bs = 0;
           bph ^= 1u;
         }
@@ -251,11 +320,15 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       }
     }
   } else if (warp < 2 + kMmaBuilderWarps) {
-    // ===== A builders: stage 1 + Hankel operand =====
+    // ===== A builders: stage 1 + Hankel rows into TMEM =====
     const int bt = tid - 64;
-    const int YF = kMmaM * TT + KP - 1;  // yf samples of an item
-    const int YL = YF + a.lf_pad - 1;    // y samples feeding them
-    unsigned a_ph = 0;
+    const int q = warp & 3;           // TMEM lane quarter
+    const int sub = (warp - 2) >> 2;  // which columns of the row this warp writes
+    const int YF = kMmaM + KP - 1;    // yf samples of an item
+    const int YL = YF + a.lf_pad - 1; // y samples feeding them
+    const int n8 = KP / 16;           // 8-column groups per part
+    const int g0 = sub ? (n8 + 1) / 2 : 0, g1 = sub ? n8 : (n8 + 1) / 2;
+    unsigned a_ph[2] = {0u, 0u};
     long long cur = -1;
     int cur_e = -1, nitem = 0;
     float chk = 0.f;
@@ -263,11 +336,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const long long item = u / nch;
       if (item == cur) continue;
       cur = item;
-      const int ti = (int)(item % a.n_titems), e = (int)(item / a.n_titems);
-      const long long T0 = (long long)ti * kMmaM * TT;
+      const int ab = nitem % NA;
+      const int e = (int)(item / gpe), ti = (int)(item % gpe) * kMmaCluster + crank;
+      const long long T0 = (long long)ti * kMmaM;
       const long long y0 = T0 - (KP - 1) - (a.lf_pad - 1);
-      PW(4, mbar_wait_sleep(a_empty, a_ph ^ 1u));  // MMAs of the previous item retired (first pass: free)
-      a_ph ^= 1u;
       if (e != cur_e)
         for (int i = bt; i < a.lf_pad; i += kMmaBuilders) s_f[i] = a.f[(long long)e * a.lf_pad + i];
       cur_e = e;
@@ -295,42 +367,47 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const int sexp = mx > 0.f ? 13 - ilogbf(mx) : 0;  // max |yf| * 2^sexp in [2^13, 2^14)
       const float scale = ldexpf(1.f, sexp);
       if (bt == 0) {
-        mbar_wait_sleep(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1));
+        PW(5, mbar_wait_sleep(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1)));
         s_sc[nitem & 1] = ldexpf(1.f, -sexp);
         mbar_arrive(&sc_full[nitem & 1]);
       }
-      // Hankel A: entry (tt, t, kc) = yf[T0 + 128 tt + t - o], o = 8 kc .. 8 kc + 7
-      const int KC = KP / 8;
+      // the MMAs that last read this A buffer must have retired
+      PW(4, mbar_wait_sleep(&a_empty[ab], a_ph[ab] ^ 1u));
+      a_ph[ab] ^= 1u;
+      tmem_fence_after();
+      {
+        // this lane's Hankel row: A[t][o] = yf[T0 + t - o], column j = {A[t][2j], A[t][2j+1]}
+        const float* src = s_yf + (32 * q + lane + KP - 1);
+        const unsigned ta = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(kMmaAccCols + ab * KP);
 #pragma unroll 1
-      for (int idx = bt; idx < TT * kMmaM * KC; idx += kMmaBuilders) {
-        const int t = idx & (kMmaM - 1);
-        const int rest = idx >> 7;
-        const int kc = rest % KC, tt = rest / KC;
-        const float* src = s_yf + (kMmaM * tt + t + KP - 1) - 8 * kc;
-        unsigned hw[4], lw[4];
+        for (int gi = g0; gi < g1; ++gi) {
+          const int j0 = 8 * gi;
+          unsigned hw[8], lw[8];
 #pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          const float x0 = src[-i] * scale, x1 = src[-i - 1] * scale;
-          const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
-          const __half l0 = __float2half_rn(x0 - __half2float(h0)), l1 = __float2half_rn(x1 - __half2float(h1));
-          hw[i / 2] = pack_half2(h0, h1);
-          lw[i / 2] = pack_half2(l0, l1);
+          for (int j = 0; j < 8; ++j) {
+            const float x0 = src[-2 * (j0 + j)] * scale, x1 = src[-2 * (j0 + j) - 1] * scale;
+            const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+            hw[j] = pack_half2(h0, h1);
+            lw[j] = pack_half2(__float2half_rn(x0 - __half2float(h0)), __float2half_rn(x1 - __half2float(h1)));
+          }
+          tmem_st8(ta + j0, hw);
+          tmem_st8(ta + KP / 2 + j0, lw);
         }
-        const int off = mma_canon(t, 8 * kc, kMmaM);
-        *reinterpret_cast<uint4*>(sA + (tt * 2 + 0) * a_part_bytes + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(sA + (tt * 2 + 1) * a_part_bytes + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        tmem_wait_st();
       }
-      fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+      tmem_fence_before();
       builders_sync();
-      if (bt == 0) mbar_arrive(a_full);
+      if (bt == 0) mbar_arrive(&a_full[ab]);
       ++nitem;
     }
     if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk)) && lane == 0) atomicOr(a.nonfinite, 1);
   } else {
-    // ===== epilogue: TMEM -> registers -> HBM =====
-    const int q = warp & 3;                                   // TMEM lane quarter of this warp
-    const int half = (warp - 2 - kMmaBuilderWarps) >> 2;      // which 32 of the chunk's 64 columns
-    float* stg = reinterpret_cast<float*>(sm + L.st_off) + (warp - 2 - kMmaBuilderWarps) * 32 * 32;
+    // ===== epilogue: TMEM -> registers -> shared staging -> TMA store =====
+    const int ew = warp - 2 - kMmaBuilderWarps;
+    const int q = warp & 3;    // TMEM lane quarter of this warp
+    const int half = ew >> 2;  // which 64 of the chunk's 128 columns
+    float* stg0 = reinterpret_cast<float*>(sm + L.st_off) + ew * 2 * 32 * 32;
+    int sbuf = 0;
     const unsigned tq = tbase + ((unsigned)(32 * q) << 16);
     int as = 0;
     unsigned aph = 0;
@@ -340,7 +417,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     for (long long u = u0; u < u1; ++u) {
       const long long item = u / nch;
       const int c = (int)(u % nch);
-      const int ti = (int)(item % a.n_titems), e = (int)(item / a.n_titems);
+      const int e = (int)(item / gpe), ti = (int)(item % gpe) * kMmaCluster + crank;
       if (item != cur) {
         if (nitem >= 0) {
           __syncwarp();
@@ -351,31 +428,34 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         unscale = s_sc[nitem & 1];
         cur = item;
       }
-      PW(5, mbar_wait_sleep(&acc_full[as], aph));
+      PW(6, mbar_wait_sleep(&acc_full[as], aph));
       tmem_fence_after();
-      const long long T0 = (long long)ti * kMmaM * TT;
-      const int d0 = c * kMmaN + 32 * half;  // this warp's 32 directions of the chunk
-      // per-direction unscale for the warp's 32 columns: lane j holds column j's factor
-      const float gsl = (d0 + lane < a.dirs ? __ldg(a.gscale + (long long)e * a.dirs_pad + d0 + lane) : 0.f) * unscale;
+      const long long t0 = (long long)ti * kMmaM + 32 * q;
+      const float unscale_c = unscale * __ldg(a.gscale + (long long)e * nch + c);  // tile 2^-s x chunk 2^-q
+      if (t0 < a.out_len) {
 #pragma unroll 1
-      for (int tt = 0; tt < TT; ++tt) {
-        const long long t0 = T0 + kMmaM * tt + 32 * q;
-        if (t0 >= a.out_len) continue;
-        if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging block
-        __syncwarp();
+        for (int blk = 0; blk < 2; ++blk) {
+          const int col = 64 * half + 32 * blk;  // accumulator column = direction within the chunk
+          const int d0 = c * kMmaN + col;
+          if (d0 >= a.dirs) break;
+          float* stg = stg0 + sbuf * 32 * 32;
+          if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer two blocks ago has read it
+          __syncwarp();
 #pragma unroll
-        for (int cb = 0; cb < 32; cb += 16) {
-          float v[16];
-          tmem_ld16(v, tq + (unsigned)(as * TT * kMmaN + tt * kMmaN + 32 * half + cb));
-          tmem_wait_ld();
+          for (int cb = 0; cb < 32; cb += 16) {
+            float v[16];
+            tmem_ld16(v, tq + (unsigned)(as * kMmaN + col + cb));
+            tmem_wait_ld();
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * __shfl_sync(0xffffffffu, gsl, cb + jj);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (elect_one()) {
-          tma_store_3d(&tm, stg, (int)t0, d0, e);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * unscale_c;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (elect_one()) {
+            tma_store_3d(&tm, stg, (int)t0, d0, e);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          sbuf ^= 1;
         }
       }
       tmem_fence_before();
@@ -386,40 +466,43 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         aph ^= 1u;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
-  if (warp >= 2 + kMmaBuilderWarps && lane == 0) bulk_wait_all();
 #if TOEP_MMA_PROF
-  if (blockIdx.x == 7 && lane == 0 && (warp <= 2 || warp == 8))
-    printf("prof cta7 warp %d total %lld: b_empty %lld a_full %lld b_full %lld acc_empty %lld a_empty %lld acc_full %lld\n",
-           warp, clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
+  if (blockIdx.x == 7 && lane == 0 && (warp <= 2 || warp == 10))
+    printf("prof cta7 warp %d total %lld: b_empty %lld a_full %lld b_full %lld acc_empty %lld a_empty %lld sc_empty %lld acc_full %lld\n",
+           warp, clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6]);
 #endif
   tmem_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc<256>(tbase);
+  cluster_sync_all();  // no CTA leaves while cluster peers may still multicast into it
+  if (warp == 0) tmem_dealloc<512>(tbase);
 }
 
-// G[e][c] chunk = [hi, lo][canonical 64 x kpad] fp16 of the dense rows of
-// directions 64c .. 64c+63, each row scaled by 2^q (max |g| * 2^q in
-// [2^13, 2^14)); gscale[e][d] = 2^-q.  One warp per (ear, direction) row.
-__global__ void k_build_gmma(const int2* __restrict__ raw, const int* __restrict__ nnz, int dirs, int ears,
-                             int stride, int kpad, int nchunks, int dirs_pad, __half* __restrict__ g,
-                             float* __restrict__ gscale) {
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= ears * dirs) return;
-  const int e = row / dirs, d = row - e * dirs;
-  const int n = nnz[row];
+// G[e][c] chunk = [hi, lo][canonical 128 x kpad] fp16 of the dense rows of
+// directions 128c .. 128c+127, scaled by 2^q with max |g| over the chunk * 2^q
+// in [2^13, 2^14); gscale[e][c] = 2^-q.  One block of kMmaN threads (one per
+// direction row) per (ear, chunk).
+__global__ void __launch_bounds__(kMmaN) k_build_gmma(const int2* __restrict__ raw, const int* __restrict__ nnz,
+                                                     int dirs, int stride, int kpad, int nchunks,
+                                                     __half* __restrict__ g, float* __restrict__ gscale) {
+  __shared__ float s_mx[kMmaN / 32];
+  const int c = blockIdx.x, e = blockIdx.y, r = threadIdx.x, d = c * kMmaN + r;
+  const bool real = d < dirs;
+  const int row = e * dirs + d;
+  const int n = real ? nnz[row] : 0;
   const int2* taps = raw + (long long)row * stride;
   float mx = 0.f;
-  for (int k = lane; k < n; k += 32) mx = fmaxf(mx, fabsf(__int_as_float(taps[k].y)));
+  for (int k = 0; k < n; ++k) mx = fmaxf(mx, fabsf(__int_as_float(taps[k].y)));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((r & 31) == 0) s_mx[r >> 5] = mx;
+  __syncthreads();
+  mx = 0.f;
+  for (int w = 0; w < kMmaN / 32; ++w) mx = fmaxf(mx, s_mx[w]);
   const int qexp = mx > 0.f ? 13 - ilogbf(mx) : 0;
-  if (lane == 0) gscale[(long long)e * dirs_pad + d] = ldexpf(1.f, -qexp);
-  const int c = d / kMmaN, r = d - c * kMmaN;
+  if (r == 0) gscale[(long long)e * nchunks + c] = ldexpf(1.f, -qexp);
   unsigned char* base = reinterpret_cast<unsigned char*>(g) + ((long long)e * nchunks + c) * 2 * kMmaN * kpad * 2;
   for (int k = 0; k < n; ++k) {  // taps are unique offsets; everything else stays zero (memset)
-    if (lane != 0) break;
     const int o = taps[k].x;
     const float x = ldexpf(__int_as_float(taps[k].y), qexp);
     const __half h = __float2half_rn(x);
@@ -430,12 +513,14 @@ __global__ void k_build_gmma(const int2* __restrict__ raw, const int* __restrict
 }
 
 int render_mma_kpad(int K) { return (K + 15) / 16 * 16; }
-int render_mma_tt(int kpad) { return kpad <= 128 ? 2 : 1; }
+int render_mma_tt(int) { return 1; }
+int render_mma_chunk() { return kMmaN; }
 
 bool render_mma_supported(int K, int lf_pad) {
   const int kp = render_mma_kpad(K);
-  if (kp > 192 || lf_pad > 512) return false;
-  return mma_smem(kp, render_mma_tt(kp), lf_pad).total <= 227 * 1024;
+  if (kp > 256 || lf_pad > 512) return false;
+  if (kMmaAccCols + kp > 512) return false;  // TMEM: accumulators + one A buffer (hi, lo)
+  return mma_smem(kp, lf_pad).total <= 227 * 1024;
 }
 
 size_t render_mma_gbytes(int ears, int dirs, int K) {
@@ -450,19 +535,38 @@ cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, i
   const int nch = (dirs + kMmaN - 1) / kMmaN;
   cudaError_t e = cudaMemsetAsync(g, 0, render_mma_gbytes(ears, dirs, K), st);
   if (e != cudaSuccess) return e;
-  const int rows = ears * dirs;
-  k_build_gmma<<<(rows + 7) / 8, 256, 0, st>>>(raw, nnz, dirs, ears, stride, kp, nch, nch * kMmaN,
-                                               reinterpret_cast<__half*>(g), gscale);
+  k_build_gmma<<<dim3(nch, ears), kMmaN, 0, st>>>(raw, nnz, dirs, stride, kp, nch, reinterpret_cast<__half*>(g),
+                                                 gscale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st) {
-  const MmaSmem L = mma_smem(a.kpad, a.tt, a.lf_pad);
+  const MmaSmem L = mma_smem(a.kpad, a.lf_pad);
   cudaError_t err = cudaFuncSetAttribute(k_render_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
-  long long grid = std::min<long long>(sm_count, a.n_units);
-  if (grid < 1) return cudaSuccess;
-  k_render_mma<<<(unsigned)grid, kMmaThreads, L.total, st>>>(a, map);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kMmaThreads);
+  cfg.dynamicSmemBytes = (size_t)L.total;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kMmaCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent: exactly the clusters that can be co-resident (GPC sizes need
+  // not be multiples of the cluster size), one CTA per SM
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cfg.gridDim = dim3((unsigned)(std::max(1, sm_count / kMmaCluster) * kMmaCluster));
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, k_render_mma, &cfg) != cudaSuccess || max_clusters < 1)
+      max_clusters = std::max(1, sm_count / kMmaCluster);
+    cudaGetLastError();
+  }
+  cfg.gridDim = dim3((unsigned)(max_clusters * kMmaCluster));
+  err = cudaLaunchKernelEx(&cfg, k_render_mma, a, map);
+  if (err != cudaSuccess) return err;
   return cudaGetLastError();
 }
 

@@ -21,7 +21,7 @@ __device__ __forceinline__ uint64_t sdesc(unsigned saddr) {
          ((uint64_t)1 << 46);
 }
 
-template <int PRODUCTS>
+template <int PRODUCTS, bool ATMEM>
 __global__ void k_probe(const float* A, const float* B, float* D) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __half* Ah = (__half*)sm;                 // [M x K] hi
@@ -32,7 +32,7 @@ __global__ void k_probe(const float* A, const float* B, float* D) {
   __shared__ unsigned tbase;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -60,6 +60,27 @@ __global__ void k_probe(const float* A, const float* B, float* D) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tmem = tbase;
+  if (ATMEM) {  // row t of A -> TMEM lane t: column j = {A[t][2j], A[t][2j+1]} (hi at col 256, lo at 256 + K/2)
+    const int t = tid;
+    for (int part = 0; part < 2; ++part)
+      for (int j0 = 0; j0 < K / 2; j0 += 8) {
+        unsigned w[8];
+        for (int j = 0; j < 8; ++j) {
+          const float x0 = A[t * K + 2 * (j0 + j)], x1 = A[t * K + 2 * (j0 + j) + 1];
+          const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+          const __half v0 = part ? __float2half_rn(x0 - __half2float(h0)) : h0;
+          const __half v1 = part ? __float2half_rn(x1 - __half2float(h1)) : h1;
+          w[j] = (unsigned)__half_as_ushort(v0) | ((unsigned)__half_as_ushort(v1) << 16);
+        }
+        const unsigned ta = tmem + ((unsigned)(32 * warp) << 16) + 256 + part * (K / 2) + j0;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(w[0]),
+                     "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]) : "memory");
+      }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
   if (tid == 0) {
     const __half* As[3] = {Ah, Ah, Al};
@@ -69,10 +90,18 @@ __global__ void k_probe(const float* A, const float* B, float* D) {
       for (int ks = 0; ks < K / 16; ++ks) {
         const uint64_t da = sdesc(su32(As[p]) + ks * M * 32);
         const uint64_t db = sdesc(su32(Bs[p]) + ks * N * 32);
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-            "l"(da), "l"(db), "r"(idesc), "r"(first ? 0 : 1));
+        if (ATMEM) {
+          const unsigned at = tmem + 256 + (p == 2 ? K / 2 : 0) + ks * 8;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+              "r"(at), "l"(db), "r"(idesc), "r"(first ? 0 : 1));
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(first ? 0 : 1));
+        }
         first = 0;
       }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
@@ -95,7 +124,7 @@ __global__ void k_probe(const float* A, const float* B, float* D) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 int main() {
@@ -109,9 +138,10 @@ int main() {
   CK(cudaMemcpy(dA, hA, M * K * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, hB, N * K * 4, cudaMemcpyHostToDevice));
   const int smem = 2 * M * K * 2 + 2 * N * K * 2;
-  for (int prods : {1, 3}) {
-    if (prods == 1) { CK(cudaFuncSetAttribute(k_probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); k_probe<1><<<1, 128, smem>>>(dA, dB, dD); }
-    else { CK(cudaFuncSetAttribute(k_probe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); k_probe<3><<<1, 128, smem>>>(dA, dB, dD); }
+  for (int prods : {1, 3, 4}) {
+    if (prods == 1) { CK(cudaFuncSetAttribute(k_probe<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); k_probe<1, false><<<1, 128, smem>>>(dA, dB, dD); }
+    else if (prods == 3) { CK(cudaFuncSetAttribute(k_probe<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); k_probe<3, false><<<1, 128, smem>>>(dA, dB, dD); }
+    else { CK(cudaFuncSetAttribute(k_probe<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); k_probe<3, true><<<1, 128, smem>>>(dA, dB, dD); }
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(hD, dD, M * N * 4, cudaMemcpyDeviceToHost));
     double num = 0, den = 0, maxe = 0;
@@ -122,7 +152,7 @@ int main() {
         const double e = hD[m * N + n] - ref;
         num += e * e; den += ref * ref; maxe = fmax(maxe, fabs(e));
       }
-    printf("products=%d  rel L2 = %.3e  max abs err = %.3e  D[0][0]=%f\n", prods, sqrt(num / den), maxe, hD[0]);
+    printf("variant=%d (4 = A from TMEM, 3 products)  rel L2 = %.3e  max abs err = %.3e  D[0][0]=%f\n", prods, sqrt(num / den), maxe, hD[0]);
   }
   return 0;
 }

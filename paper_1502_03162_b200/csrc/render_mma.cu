@@ -69,7 +69,14 @@ constexpr int kMmaEpiWarps = 8;      // two per TMEM lane quarter (64 columns ea
 constexpr int kMmaWarps = 2 + kMmaBuilderWarps + kMmaEpiWarps;
 constexpr int kMmaThreads = 32 * kMmaWarps;
 constexpr int kMmaBuilders = 32 * kMmaBuilderWarps;
-constexpr int kMmaBStages = 2;
+#ifndef TOEP_MMA_BSTAGES
+#define TOEP_MMA_BSTAGES 2
+#endif
+#ifndef TOEP_MMA_STGBUF
+#define TOEP_MMA_STGBUF 2
+#endif
+constexpr int kMmaBStages = TOEP_MMA_BSTAGES;
+constexpr int kMmaStgBuf = TOEP_MMA_STGBUF;  // epilogue staging buffers per warp
 #ifndef TOEP_MMA_CLUSTER
 #define TOEP_MMA_CLUSTER 4
 #endif
@@ -166,7 +173,7 @@ __host__ __device__ inline MmaSmem mma_smem(int kpad, int lf_pad) {
   L.b_off = 0;  // [kMmaBStages][hi, lo][canonical 128 x kpad] fp16
   int off = kMmaBStages * 2 * kMmaN * kpad * 2;
   L.st_off = off;  // epilogue staging: [epilogue warps][2 buffers][32 directions][32 t] fp32
-  off += kMmaEpiWarps * 2 * 32 * 32 * 4;
+  off += kMmaEpiWarps * kMmaStgBuf * 32 * 32 * 4;
   L.y_off = off;
   off += ((kMmaM + kpad + lf_pad + 31) & ~31) * 4;
   L.yf_off = off;
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     const int ew = warp - 2 - kMmaBuilderWarps;
     const int q = warp & 3;    // TMEM lane quarter of this warp
     const int half = ew >> 2;  // which 64 of the chunk's 128 columns
-    float* stg0 = reinterpret_cast<float*>(sm + L.st_off) + ew * 2 * 32 * 32;
+    float* stg0 = reinterpret_cast<float*>(sm + L.st_off) + ew * kMmaStgBuf * 32 * 32;
     int sbuf = 0;
     const unsigned tq = tbase + ((unsigned)(32 * q) << 16);
     int as = 0;
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
           const int d0 = c * kMmaN + col;
           if (d0 >= a.dirs) break;
           float* stg = stg0 + sbuf * 32 * 32;
-          if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer two blocks ago has read it
+          if (lane == 0) bulk_wait_read<kMmaStgBuf - 1>();  // the store that last used this buffer has read it
           __syncwarp();
 #pragma unroll
           for (int cb = 0; cb < 32; cb += 16) {
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             tma_store_3d(&tm, stg, (int)t0, d0, e);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          sbuf ^= 1;
+          if (++sbuf == kMmaStgBuf) sbuf = 0;
         }
       }
       tmem_fence_before();

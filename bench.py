@@ -388,7 +388,10 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
     flops = 2.0 * int(br.row_nnz.sum()) * (cfg.ny + cfg.lf - 1) + 2.0 * cfg.ears * cfg.lf * (cfg.ny + br.M)
     roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": _traffic(workload),
-            "peak_src": peaks["src"], "kernel": "k_render<112,true,16>",
+            "peak_src": peaks["src"],
+            "kernel": {"tensor": "k_render_mma (tcgen05.mma split-fp16, TMA-multicast G)",
+                       "window": "k_render<112,true,16> (TMEM window + FFMA2)",
+                       "banded": "k_sparse_generic"}[br.native.path()],
             "fp32_tflops": flops / (kern_ms * 1e-3) / 1e12,
             "alg_bytes_per_launch": alg_bytes}
 

@@ -84,6 +84,15 @@ int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny);
  * ref: Renderer.render (engine/__init__.py:238-260) for all directions. */
 int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, float* out, int64_t out_pitch,
                          void* stream);
+/* Kernel toep_renderer_render uses for this renderer:
+ * TOEP_PATH_TENSOR  -- stage 2 as a split-fp16 GEMM on the tensor cores (tcgen05.mma)
+ * TOEP_PATH_WINDOW  -- TMEM sliding window + FFMA2 per sparse tap
+ * TOEP_PATH_BANDED  -- banded shared-memory kernel (reflection length > 497)
+ * (TOEP_RENDER_MMA=0 in the environment disables the tensor path.) */
+#define TOEP_PATH_TENSOR 1
+#define TOEP_PATH_WINDOW 0
+#define TOEP_PATH_BANDED 2
+int toep_renderer_path(const toep_renderer* r);
 /* Fused input check (the reference's DataError "signal contains non-finite
  * samples", engine/__init__.py:162-165): every render / reflect / mixer /
  * streamer kernel made from this renderer ORs a device flag when it reads an

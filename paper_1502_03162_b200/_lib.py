@@ -24,7 +24,7 @@ EXPORTS = (
     "toep_conv_dense", "toep_conv_sparse",
     "toep_taps_create", "toep_taps_destroy", "toep_taps_info", "toep_taps_conv",
     "toep_renderer_create", "toep_renderer_destroy", "toep_renderer_out_len", "toep_renderer_min_pitch",
-    "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check",
+    "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check", "toep_renderer_path",
     "toep_mixer_create", "toep_mixer_destroy", "toep_mixer_z_len", "toep_mixer_out_len",
     "toep_mixer_partial", "toep_mixer_finish",
     "toep_streamer_create", "toep_streamer_destroy", "toep_streamer_reset", "toep_streamer_step",
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
         "toep_renderer_render": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
         "toep_renderer_reflect": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp, _i64, _vp]),
         "toep_renderer_check": (ctypes.c_int, [_vp, _i32p, _vp]),
+        "toep_renderer_path": (ctypes.c_int, [_vp]),
         "toep_mixer_create": (ctypes.c_int, [_vp, _i32p, _i32, _i64, ctypes.POINTER(_vp)]),
         "toep_mixer_destroy": (ctypes.c_int, [_vp]),
         "toep_mixer_z_len": (_i64, [_vp]),
@@ -214,6 +215,12 @@ class NativeRenderer:
     def render(self, y, out, pitch: int, stream=None):
         check(load_library().toep_renderer_render(self._h, dptr(y), int(y.numel()), dptr(out), int(pitch),
                                                   stream_ptr(stream)))
+
+    PATHS = {1: "tensor", 0: "window", 2: "banded"}
+
+    def path(self) -> str:
+        """Which stage-2 kernel render() launches: "tensor" (tcgen05 GEMM), "window" (TMEM + FFMA2), "banded"."""
+        return self.PATHS[load_library().toep_renderer_path(self._h)]
 
     def clear_nonfinite(self, stream=None):
         check(load_library().toep_renderer_check(self._h, None, stream_ptr(stream)))

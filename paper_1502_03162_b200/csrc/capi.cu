@@ -412,6 +412,18 @@ int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny) {
   return r ? round_up(toep_renderer_out_len(r, ny), 4) : -1;
 }
 
+// tensor-core path unless the taps are so sparse (<= 8 per row) that the FFMA
+// kernel already meets the write roofline while the GEMM pays for KPAD > 128
+// zero columns (cfg3 sweep)
+static int renderer_path(const toep_renderer* r) {
+  const toep_taps* g = r->g;
+  if (r->d_gmma && render_mma_enabled() && !(g->max_nnz <= 8 && render_mma_kpad(g->length) > 128))
+    return TOEP_PATH_TENSOR;
+  return g->kwin > 0 ? TOEP_PATH_WINDOW : TOEP_PATH_BANDED;
+}
+
+int toep_renderer_path(const toep_renderer* r) { return r ? renderer_path(r) : -1; }
+
 int toep_renderer_check(const toep_renderer* r, int32_t* nonfinite, void* stream) {
   if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
   cudaStream_t st = S(stream);
@@ -437,7 +449,7 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
   if (rows > 1 && out_pitch < out_len) return fail(TOEP_ERR_INVALID, "output pitch %lld < %lld", (long long)out_pitch, out_len);
   cudaStream_t st = S(stream);
   const toep_taps* g = r->g;
-  if (r->d_gmma && render_mma_enabled()) {
+  if (renderer_path(r) == TOEP_PATH_TENSOR) {
     if (!aligned16(out) || (rows > 1 && out_pitch % 4 != 0))
       return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");
     RenderMmaArgs a{};

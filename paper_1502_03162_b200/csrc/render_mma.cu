@@ -72,11 +72,8 @@ constexpr int kMmaBuilders = 32 * kMmaBuilderWarps;
 #ifndef TOEP_MMA_BSTAGES
 #define TOEP_MMA_BSTAGES 2
 #endif
-#ifndef TOEP_MMA_STGBUF
-#define TOEP_MMA_STGBUF 2
-#endif
 constexpr int kMmaBStages = TOEP_MMA_BSTAGES;
-constexpr int kMmaStgBuf = TOEP_MMA_STGBUF;  // epilogue staging buffers per warp
+
 #ifndef TOEP_MMA_CLUSTER
 #define TOEP_MMA_CLUSTER 4
 #endif
@@ -165,15 +162,15 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const float*
 }
 
 struct MmaSmem {
-  int b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total;
+  int b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total, nstg;
 };
 
-__host__ __device__ inline MmaSmem mma_smem(int kpad, int lf_pad) {
+__host__ __device__ inline MmaSmem mma_smem_n(int kpad, int lf_pad, int nstg) {
   MmaSmem L{};
   L.b_off = 0;  // [kMmaBStages][hi, lo][canonical 128 x kpad] fp16
   int off = kMmaBStages * 2 * kMmaN * kpad * 2;
-  L.st_off = off;  // epilogue staging: [epilogue warps][2 buffers][32 directions][32 t] fp32
-  off += kMmaEpiWarps * kMmaStgBuf * 32 * 32 * 4;
+  L.st_off = off;  // epilogue staging: [epilogue warps][nstg buffers][32 directions][32 t] fp32
+  off += kMmaEpiWarps * nstg * 32 * 32 * 4;
   L.y_off = off;
   off += ((kMmaM + kpad + lf_pad + 31) & ~31) * 4;
   L.yf_off = off;
@@ -187,7 +184,14 @@ __host__ __device__ inline MmaSmem mma_smem(int kpad, int lf_pad) {
   L.bars_off = off;
   off += (12 + 2 * kMmaBStages) * 8;
   L.total = off + 1024;  // alignment slack
+  L.nstg = nstg;
   return L;
+}
+
+// double-buffered epilogue staging when it fits next to the G ring, else single
+__host__ __device__ inline MmaSmem mma_smem(int kpad, int lf_pad) {
+  const MmaSmem L2 = mma_smem_n(kpad, lf_pad, 2);
+  return L2.total <= 227 * 1024 ? L2 : mma_smem_n(kpad, lf_pad, 1);
 }
 
 // A buffers in TMEM after the two accumulators: two when they fit (the next
@@ -413,7 +417,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     const int ew = warp - 2 - kMmaBuilderWarps;
     const int q = warp & 3;    // TMEM lane quarter of this warp
     const int half = ew >> 2;  // which 64 of the chunk's 128 columns
-    float* stg0 = reinterpret_cast<float*>(sm + L.st_off) + ew * kMmaStgBuf * 32 * 32;
+    const int nstg = L.nstg;
+    float* stg0 = reinterpret_cast<float*>(sm + L.st_off) + ew * nstg * 32 * 32;
     int sbuf = 0;
     const unsigned tq = tbase + ((unsigned)(32 * q) << 16);
     int as = 0;
@@ -446,7 +451,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
           const int d0 = c * kMmaN + col;
           if (d0 >= a.dirs) break;
           float* stg = stg0 + sbuf * 32 * 32;
-          if (lane == 0) bulk_wait_read<kMmaStgBuf - 1>();  // the store that last used this buffer has read it
+          if (lane == 0) {  // the store that last used this buffer has read it
+            if (nstg == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
 #pragma unroll
           for (int cb = 0; cb < 32; cb += 16) {
@@ -462,7 +470,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             tma_store_3d(&tm, stg, (int)t0, d0, e);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          if (++sbuf == kMmaStgBuf) sbuf = 0;
+          if (++sbuf == nstg) sbuf = 0;
         }
       }
       tmem_fence_before();

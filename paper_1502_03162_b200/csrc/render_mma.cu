@@ -75,9 +75,9 @@ constexpr int kMmaBuilders = 32 * kMmaBuilderWarps;
 constexpr int kMmaBStages = TOEP_MMA_BSTAGES;
 
 #ifndef TOEP_MMA_CLUSTER
-#define TOEP_MMA_CLUSTER 4
+#define TOEP_MMA_CLUSTER 6
 #endif
-constexpr int kMmaCluster = TOEP_MMA_CLUSTER;  // CTAs sharing each G chunk load (TMA multicast)
+constexpr int kMmaCluster = TOEP_MMA_CLUSTER;  // CTAs sharing each G chunk load (TMA multicast); 6 measured best of 1-8
 constexpr int kMmaAccCols = 2 * kMmaN;  // accumulators: 2 buffers x 128 columns; A buffers follow
 
 // byte offset of element (r, k) in an R-row, K-major, SWIZZLE_NONE canonical
@@ -274,10 +274,11 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         const int e = (int)(u / nch / gpe);
         PW(0, mbar_wait_sleep(&b_empty[bs], bph ^ 1u));  // the stage is free in every CTA of the cluster
         mbar_arrive_expect_tx(&b_full[bs], (unsigned)b_chunk_bytes);
-        const int slice = b_chunk_bytes / kMmaCluster;  // this CTA loads one slice for the whole cluster
-        bulk_load_multicast(sB + bs * b_chunk_bytes + crank * slice,
-                            g + ((long long)e * nch + c) * b_chunk_bytes + crank * slice, (unsigned)slice,
-                            &b_full[bs], cmask);
+        // this CTA loads one 16-byte-aligned slice of the chunk for the whole cluster
+        const int sl0 = (int)((long long)b_chunk_bytes / 16 * crank / kMmaCluster) * 16;
+        const int sl1 = (int)((long long)b_chunk_bytes / 16 * (crank + 1) / kMmaCluster) * 16;
+        bulk_load_multicast(sB + bs * b_chunk_bytes + sl0, g + ((long long)e * nch + c) * b_chunk_bytes + sl0,
+                            (unsigned)(sl1 - sl0), &b_full[bs], cmask);
         if (++bs == kMmaBStages) {
           bs = 0;
           bph ^= 1u;

@@ -49,8 +49,14 @@ def main():
         bytes_ = 4.0 * samples + 4 * cfg.ny
         hbm_frac = bytes_ / t / (peaks["hbm_gbs"] * 1e9)
         fma_frac = flops / t / fp32
-        bound = "hbm" if flops / bytes_ < fp32 / (peaks["hbm_gbs"] * 1e9) else "fp32"
-        line = {"point": cfg.name, "K": cfg.K, "nnz": cfg.nnz, "Lf": cfg.lf, "ms": t * 1e3,
+        path = br.native.path()
+        # the tensor-core path executes the dense GEMM far below its tensor peak, so
+        # the output write stream binds it; the FFMA paths bind at HBM or FP32
+        if path == "tensor":
+            bound = "hbm"
+        else:
+            bound = "hbm" if flops / bytes_ < fp32 / (peaks["hbm_gbs"] * 1e9) else "fp32"
+        line = {"point": cfg.name, "K": cfg.K, "nnz": cfg.nnz, "Lf": cfg.lf, "path": path, "ms": t * 1e3,
                 "samples_per_s": samples / t, "bound": bound, "hbm_frac": hbm_frac, "fp32_frac": fma_frac,
                 "roofline_frac": hbm_frac if bound == "hbm" else fma_frac}
         if args.check:

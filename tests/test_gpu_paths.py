@@ -80,3 +80,31 @@ def test_tensor_path_small_and_large_magnitudes(mods):
         ref = oracle.render_rows(y, f, model_rows(ms), cfg.K, cfg.dirs, rows=np.array([0, 21, 39], np.int32))
         for i, r in enumerate((0, 21, 39)):
             assert rel_l2(out[r], ref[i]) <= TOL, (scale, r)
+
+
+@pytest.mark.parametrize("K,lf,dirs,ears", [(1, 1, 1, 1), (2, 3, 3, 2), (16, 1, 2, 1), (17, 40, 5, 2), (33, 7, 130, 1),
+                                            (128, 73, 4, 2), (129, 20, 3, 2), (192, 9, 2, 1), (200, 1, 2, 2),
+                                            (256, 5, 3, 1), (257, 5, 2, 1), (498, 3, 2, 1)])
+def test_shape_envelope(mods, K, lf, dirs, ears):
+    """Reflection lengths across every kernel boundary (KPAD 16..256, the
+    window kernel's KWIN tiers, the banded fallback), tiny resonance filters,
+    one ear, a single direction and partial 128-direction chunks."""
+    batch, synth, model_rows = mods
+    from paper_1502_03162_b200 import FactorizedModel, SparseFilter
+    rng = np.random.default_rng(K * 31 + lf)
+    models = []
+    for e in range(ears):
+        refl = []
+        for d in range(dirs):
+            n = int(rng.integers(1, min(K, 24) + 1))
+            idx = np.sort(rng.choice(K, size=n, replace=False)).astype(np.int64)
+            refl.append(SparseFilter(idx, np.abs(rng.standard_normal(n)) + 0.05, K))
+        models.append(FactorizedModel(rng.standard_normal(lf), refl))
+    br = batch.BatchRenderer(models)
+    f = np.stack([m.resonance_taps for m in models])
+    for ny in (1, 300, 4097):
+        y = synth.source(ny, seed=ny + K)
+        out = br.render_all(y).reshape(ears * dirs, -1).cpu().numpy()
+        ref = oracle.render_rows(y, f, model_rows(models), K, dirs)
+        for r in range(ears * dirs):
+            assert rel_l2(out[r], ref[r]) <= TOL, (ny, r, br.native.path())

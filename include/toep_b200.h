@@ -57,6 +57,18 @@ int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps
 int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const float* values, int64_t nnz,
                      int64_t length, float* out, int64_t* macs, void* stream);
 
+/* Power-of-two DFT of n complex128 values (interleaved re, im), inverse
+ * scaled by 1/n.  ref: _kernels.pyx:47-77 (fft); *macs = n/2 * log2(n).
+ * in may equal out. */
+int toep_fft(const double* in, double* out, int64_t n, int inverse, int64_t* macs, void* stream);
+/* spectrum[n] (complex64, interleaved) = DFT of taps[0..ntaps) zero-padded to n. */
+int toep_fft_spectrum(const float* taps, int64_t ntaps, int64_t n, float* spectrum, void* stream);
+/* FFT overlap-save: out[0 .. ny+ntaps-1) = y * taps, blocks of n samples
+ * advancing by n - ntaps + 1, with spectrum from toep_fft_spectrum.
+ * ref: engine/__init__.py:178-205 (_overlap_save). */
+int toep_fft_conv(const float* y, int64_t ny, const float* spectrum, int64_t n, int64_t ntaps, float* out,
+                  void* stream);
+
 /* ---- tap tables (ConvPlan.sparse_parts / SparseFilter, device resident) - */
 typedef struct toep_taps toep_taps;
 /* rows CSR filters of common dense length `length`, HOST arrays:

@@ -55,15 +55,16 @@ def conv_sparse(y, indices, values, length):
 
 
 def fft(data, bitrev, twiddles, inverse):
-    """Power-of-two DFT (ref: _kernels.pyx:47-77), computed with cuFFT in complex128.
+    """Power-of-two DFT (ref: _kernels.pyx:47-77): radix-2 in complex128 on the GPU (fft.cu).
 
-    ``bitrev``/``twiddles`` are accepted for signature compatibility; ``macs``
-    counts radix-2 butterflies, n/2 * log2(n), as the reference does.
+    ``bitrev``/``twiddles`` are accepted for signature compatibility (the
+    kernel derives both); ``macs`` counts radix-2 butterflies, n/2 * log2(n),
+    as the reference does.
     """
     t = _lib.require_cuda()
     is_t = isinstance(data, t.Tensor)
-    d = data.to("cuda", t.complex128) if is_t else t.from_numpy(np.ascontiguousarray(data, np.complex128)).cuda()
-    n = d.numel()
-    out = t.fft.ifft(d) if inverse else t.fft.fft(d)
-    macs = (n // 2) * (n.bit_length() - 1) if n > 1 else 0
+    d = data.to("cuda", t.complex128).contiguous() if is_t else \
+        t.from_numpy(np.ascontiguousarray(data, np.complex128)).cuda()
+    out = t.empty_like(d)
+    macs = _lib.fft_c128(d, out, bool(inverse))
     return (out if is_t else out.cpu().numpy()), macs

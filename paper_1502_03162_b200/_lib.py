@@ -21,7 +21,7 @@ TOEP_OK, TOEP_ERR_INVALID, TOEP_ERR_CUDA, TOEP_ERR_NOMEM, TOEP_ERR_UNSUPPORTED =
 #: every function declared in include/toep_b200.h
 EXPORTS = (
     "toep_last_error", "toep_abi_version", "toep_sm_count",
-    "toep_conv_dense", "toep_conv_sparse",
+    "toep_conv_dense", "toep_conv_sparse", "toep_fft", "toep_fft_spectrum", "toep_fft_conv",
     "toep_taps_create", "toep_taps_destroy", "toep_taps_info", "toep_taps_conv",
     "toep_renderer_create", "toep_renderer_destroy", "toep_renderer_out_len", "toep_renderer_min_pitch",
     "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check", "toep_renderer_path",
@@ -65,6 +65,9 @@ def load_library(path: str = LIB_PATH):
         "toep_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
         "toep_conv_dense": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64p, _vp]),
         "toep_conv_sparse": (ctypes.c_int, [_vp, _i64, _i64p, _fp, _i64, _i64, _vp, _i64p, _vp]),
+        "toep_fft": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.POINTER(_i64), _vp]),
+        "toep_fft_spectrum": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp]),
+        "toep_fft_conv": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _vp]),
         "toep_taps_create": (ctypes.c_int, [_i32, _i32, _i64p, _i64p, _fp, ctypes.POINTER(_vp)]),
         "toep_taps_destroy": (ctypes.c_int, [_vp]),
         "toep_taps_info": (ctypes.c_int, [_vp, _i32p, _i32p, _i32p, _i64p]),
@@ -317,3 +320,25 @@ def conv_sparse_dev(y, indices: np.ndarray, values: np.ndarray, length: int, out
                                           val.ctypes.data_as(_fp), idx.size, int(length), dptr(out),
                                           ctypes.byref(macs), stream_ptr(stream)))
     return int(macs.value)
+
+
+def fft_c128(x, out, inverse: bool, stream=None) -> int:
+    """out = DFT of x (complex128 CUDA tensors, power-of-two length); returns the butterfly count."""
+    macs = _i64()
+    check(load_library().toep_fft(dptr(x), dptr(out), int(x.numel()), 1 if inverse else 0, ctypes.byref(macs),
+                                  stream_ptr(stream)))
+    return int(macs.value)
+
+
+def fft_spectrum(taps, n: int, stream=None):
+    """complex64 CUDA tensor [n]: DFT of the float32 taps zero-padded to n."""
+    t = torch()
+    spec = t.empty(n, device="cuda", dtype=t.complex64)
+    check(load_library().toep_fft_spectrum(dptr(taps), int(taps.numel()), int(n), dptr(spec), stream_ptr(stream)))
+    return spec
+
+
+def fft_conv(y, spectrum, n: int, ntaps: int, out, stream=None) -> None:
+    """FFT overlap-save convolution of float32 y with the taps behind ``spectrum`` into out."""
+    check(load_library().toep_fft_conv(dptr(y), int(y.numel()), dptr(spectrum), int(n), int(ntaps), dptr(out),
+                                       stream_ptr(stream)))

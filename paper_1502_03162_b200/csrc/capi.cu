@@ -318,6 +318,58 @@ int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const f
 
 }  // extern "C"
 
+// ------------------------------------------------------------------ FFT ----
+static bool pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+extern "C" {
+
+int toep_fft(const double* in, double* out, int64_t n, int inverse, int64_t* macs, void* stream) {
+  if (!pow2(n)) return fail(TOEP_ERR_INVALID, "transform length must be a power of two, got %lld", (long long)n);
+  if (!in || !out) return fail(TOEP_ERR_INVALID, "null buffer");
+  cudaStream_t st = S(stream);
+  int logn = 0;
+  while ((1LL << logn) < n) ++logn;
+  if (macs) *macs = n > 1 ? (n / 2) * logn : 0;  // butterflies, _kernels.pyx:72
+  double* dst = out;
+  double* tmp = nullptr;
+  if (in == out && fft_needs_distinct(n, true)) {
+    TOEP_CUDA(cudaMallocAsync(&tmp, (size_t)n * 2 * sizeof(double), st));
+    dst = tmp;
+  }
+  cudaError_t e = launch_fft_c128(in, dst, n, inverse != 0, st);
+  if (e == cudaSuccess && tmp) e = cudaMemcpyAsync(out, tmp, (size_t)n * 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (tmp) cudaFreeAsync(tmp, st);
+  return e == cudaSuccess ? TOEP_OK : cuda_fail(e, "toep_fft");
+}
+
+int toep_fft_spectrum(const float* taps, int64_t ntaps, int64_t n, float* spectrum, void* stream) {
+  if (!pow2(n)) return fail(TOEP_ERR_INVALID, "transform length must be a power of two, got %lld", (long long)n);
+  if (ntaps < 1 || ntaps > n || !taps || !spectrum) return fail(TOEP_ERR_INVALID, "bad taps for a %lld-point spectrum", (long long)n);
+  cudaStream_t st = S(stream);
+  float* tmp = nullptr;
+  TOEP_CUDA(cudaMallocAsync(&tmp, (size_t)n * 2 * sizeof(float), st));
+  cudaError_t e = launch_fft_spectrum(taps, ntaps, n, spectrum, tmp, st);
+  cudaFreeAsync(tmp, st);
+  return e == cudaSuccess ? TOEP_OK : cuda_fail(e, "toep_fft_spectrum");
+}
+
+int toep_fft_conv(const float* y, int64_t ny, const float* spectrum, int64_t n, int64_t ntaps, float* out,
+                  void* stream) {
+  if (ny < 1 || !y) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
+  if (!pow2(n) || n < 2) return fail(TOEP_ERR_INVALID, "block size must be a power of two >= 2, got %lld", (long long)n);
+  if (ntaps < 1 || ntaps > n) return fail(TOEP_ERR_INVALID, "block size %lld is smaller than the %lld-tap filter", (long long)n, (long long)ntaps);
+  if (!spectrum || !out) return fail(TOEP_ERR_INVALID, "null buffer");
+  cudaStream_t st = S(stream);
+  const long long sb = fft_conv_scratch_bytes(ny, n, ntaps);
+  float* scratch = nullptr;
+  if (sb > 0) TOEP_CUDA(cudaMallocAsync(&scratch, (size_t)sb, st));
+  cudaError_t e = launch_fft_conv(y, ny, spectrum, n, ntaps, out, scratch, st);
+  if (scratch) cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? TOEP_OK : cuda_fail(e, "toep_fft_conv");
+}
+
+}  // extern "C"
+
 // -------------------------------------------------------------- renderer ----
 struct toep_renderer {
   int ears = 0, lf = 0, lf_pad = 0, dirs = 0, pairs_per_ear = 0;

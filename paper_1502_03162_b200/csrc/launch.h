@@ -68,6 +68,16 @@ cudaError_t make_render_mma_map(float* out, int ears, int dirs, long long out_le
                                 CUtensorMap* m);
 cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st);
 
+// FFT (fft.cu): radix-2, power-of-two n; complex buffers interleaved.
+cudaError_t launch_fft_c128(const double* in, double* out, long long n, bool inverse, cudaStream_t st);
+cudaError_t launch_fft_c64(const float* in, float* out, long long n, long long batch, bool inverse, cudaStream_t st);
+cudaError_t launch_fft_conv(const float* y, long long ny, const float* spectrum, long long n, long long ntaps,
+                            float* out, float* scratch, cudaStream_t st);
+cudaError_t launch_fft_spectrum(const float* taps, long long ntaps, long long n, float* spectrum, float* tmp,
+                                cudaStream_t st);
+long long fft_conv_scratch_bytes(long long ny, long long n, long long ntaps);
+bool fft_needs_distinct(long long n, bool dbl);
+
 // TMA tensor maps over the output rows ([rows][out_len], row stride out_pitch):
 // box {256, 2} for direction pairs and {256, 1} for a trailing odd direction.
 struct RenderMaps {

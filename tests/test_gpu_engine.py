@@ -209,3 +209,39 @@ class TestBench:
         lines = open(path).read().splitlines()
         assert lines[0] == eng.BENCH_CSV_HEADER + ",backend"
         assert len(lines) == 1 + len(rows)
+
+
+class TestFftKernels:
+    """fft.cu: complex128 plugin transform across the shared-memory / global
+    boundary, and the complex64 overlap-save convolution for every block size
+    the reference allows (engine/__init__.py:104-139) up to the global path."""
+
+    @pytest.mark.parametrize("n", [1, 2, 4, 128, 8192, 16384, 1 << 18])
+    def test_fft_sizes(self, eng, n):
+        rng = np.random.default_rng(n)
+        data = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        got = eng.radix2_fft(data)
+        ref = np.fft.fft(data)
+        assert np.max(np.abs(got - ref)) <= 1e-9 * max(1.0, np.max(np.abs(ref)))
+        back = eng.radix2_fft(got, inverse=True)
+        assert np.max(np.abs(back - data)) <= 1e-11 * max(1.0, np.max(np.abs(data)))
+
+    def test_fft_in_place_abi(self, eng, cuda):
+        from paper_1502_03162_b200 import _lib
+        torch = cuda
+        for n in (64, 1 << 15):
+            x = torch.randn(n, dtype=torch.complex128, device="cuda")
+            ref = torch.fft.fft(x)
+            y = x.clone()
+            assert _lib.fft_c128(y, y, False) == (n // 2) * (n.bit_length() - 1)
+            assert float((y - ref).abs().max()) <= 1e-9 * float(ref.abs().max())
+
+    @pytest.mark.parametrize("ntaps,block", [(3, None), (100, None), (100, 128), (200, 1 << 13), (5000, None),
+                                             (9000, 1 << 16)])
+    def test_overlap_save_blocks(self, eng, ntaps, block):
+        rng = np.random.default_rng(ntaps)
+        taps = rng.uniform(0.5, 1.5, size=ntaps)
+        y = rng.standard_normal(70_000)
+        plan = eng.ConvPlan(taps, "fft_overlap_save", block_size=block)
+        got = eng.convolve(plan, y)
+        assert rel_l2(got, np.convolve(y, taps)) < TOL

@@ -4,6 +4,7 @@
     # then on the GPU: TOEP_LIB=paper_1502_03162_b200/build/variants/libtoep_NAME.so python bench.py ...
 """
 import os
+import shutil
 import subprocess
 import sys
 
@@ -28,6 +29,7 @@ def build_variant(name, defines):
             raise SystemExit("nvcc failed for " + name)
     lib = os.path.join(OUT, "libtoep_%s.so" % name)
     subprocess.check_call([_build._nvcc(), *_build.NVCC_FLAGS, "-shared", *objs, "-o", lib])
+    shutil.rmtree(os.path.join(OUT, name))  # objects are not needed on the GPU box
     print(lib)
 
 

@@ -136,9 +136,7 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st) {
 // No CTA barrier inside the bucket loop (only when the group's tables
 // change), so warps drift freely; partials leave once per item.
 constexpr int kMixMaxBuckets = 512;   // buckets per group (shared-memory tables)
-#ifndef TOEP_MIX_UNROLL_SLOTS
-#define TOEP_MIX_UNROLL_SLOTS 1
-#endif
+
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -256,14 +254,9 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       cp_async_wait_all();
       if (interior) {
         const int n = min(i1 - i0, SLOTS);
-#if TOEP_MIX_UNROLL_SLOTS
 #pragma unroll
         for (int u = 0; u < SLOTS; ++u) {  // all slot loads can issue before the adds
           if (u < n) {
-#else
-        for (int u = 0; u < n; ++u) {
-          {
-#endif
 #pragma unroll
             for (int q = 0; q < V4; ++q) {
               const int c = lane + 32 * q;

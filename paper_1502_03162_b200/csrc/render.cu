@@ -106,16 +106,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const float*
                : "memory");
 }
 
-// SPLIT: 8 warps, two per TMEM lane quarter, sharing the quarter's windows;
-// warp (q, sub) renders direction 2p+sub of every pair p as one FFMA2 chain
-// (half the registers of the paired chain, twice the warps to hide TMEM/LDS
-// latency).  !SPLIT: 4 warps, each renders both directions of a pair.
-template <int KWIN, bool STAGE1, int NNZT, bool SPLIT>
-__global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
+template <int KWIN, bool STAGE1, int NNZT>
+__global__ void __launch_bounds__(kThreads,
                                   (512 / (kR + KWIN)) > 3 ? TOEP_RENDER_MINB : (512 / (kR + KWIN)))
     k_render(RenderArgs a, const __grid_constant__ CUtensorMap tm2, const __grid_constant__ CUtensorMap tm1) {
   using C = RenderCfg<KWIN>;
-  constexpr int NW = SPLIT ? 2 * kWarps : kWarps;
+  constexpr int NW = kWarps;
   constexpr int NT = 32 * NW;
   extern __shared__ float smem_raw[];
   __shared__ unsigned s_tbase;
@@ -146,7 +142,7 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const int quarter = warp & 3, sub = SPLIT ? (warp >> 2) : 0;
+  const int quarter = warp & 3;
   const unsigned tlane = s_tbase + ((unsigned)(32 * quarter) << 16);
 
   UnitMap um;
@@ -210,7 +206,7 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
         for (int i = tid; i < C::YH; i += NT) s_yf[i] = s_halo[i];
       __syncthreads();
       if (!reuse_halo) {
-        for (int c = SPLIT ? tid - kThreads : tid; c >= 0 && c < C::YH / 16; c += kThreads) {
+        for (int c = tid; c < C::YH / 16; c += kThreads) {
           float acc[16];
 #pragma unroll
           for (int r = 0; r < 16; ++r) acc[r] = 0.f;
@@ -245,9 +241,8 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
     // ---- lane windows -> TMEM; keep the next tile's halo -----------------
     {
       const int wbase = (C::YH - KWIN) + 16 * (32 * quarter + lane);  // = 16 + 16*lane row
-      constexpr int CW = SPLIT ? C::COLS / 2 : C::COLS;              // columns written by this warp
 #pragma unroll
-      for (int c = sub * CW; c < (sub + 1) * CW; c += 16) {
+      for (int c = 0; c < C::COLS; c += 16) {
         float v[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -283,39 +278,7 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
       }
       const int4* tp = s_ring + (buf * CP + kin) * a.tap_stride;
       float accA[16], accB[16];
-      if constexpr (SPLIT) {
-        // one row: direction 2p + sub, taps are the (sub) half of each int4
-        const int2* tq = reinterpret_cast<const int2*>(tp) + sub;
-        const int nk = NNZT > 0 ? NNZT : (sub ? s_rnnz[buf * CP + kin].y : s_rnnz[buf * CP + kin].x);
-        if (nk == 0) {
-#pragma unroll
-          for (int r = 0; r < 16; ++r) accA[r] = 0.f;
-        } else {
-          float X0[16], X1[16];
-          int2 t = tq[0];
-          int2 tn = tq[2 * min(1, nk - 1)];
-          tmem_ld16(X0, tlane + t.x);
-#pragma unroll(NNZT > 0 ? NNZT : 2)
-          for (int k = 0; k < nk; ++k) {
-            const int2 tnn = tq[2 * min(k + 2, nk - 1)];
-            float(&X)[16] = (k & 1) ? X1 : X0;
-            float(&Y)[16] = (k & 1) ? X0 : X1;
-            const unsigned na = tlane + tn.x;
-            tmem_wait_ld();
-            if (k + 1 < nk) tmem_ld16(Y, na);
-            const float v = __int_as_float(t.y);
-            if (k == 0) {
-#pragma unroll
-              for (int r = 0; r < 16; r += 2) fmul2(accA[r], accA[r + 1], X[r], X[r + 1], v);
-            } else {
-#pragma unroll
-              for (int r = 0; r < 16; r += 2) ffma2(accA[r], accA[r + 1], X[r], X[r + 1], v);
-            }
-            t = tn;
-            tn = tnn;
-          }
-        }
-      } else if constexpr (NNZT > 0) {
+      if constexpr (NNZT > 0) {
         // software pipeline: the TMEM loads of tap k+1 are in flight while
         // tap k's 32 FFMA issue (tcgen05.wait::ld only ever waits for tap k)
         float XA0[16], XB0[16], XA1[16], XB1[16];
@@ -388,28 +351,7 @@ __global__ void __launch_bounds__(kThreads * (SPLIT ? 2 : 1),
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
       }
-      if constexpr (SPLIT) {
-        float* row = st + pp * 512;  // [pp][512]
-#pragma unroll
-        for (int r = 0; r < 16; r += 4)
-          *reinterpret_cast<float4*>(&row[16 * lane + r]) = make_float4(accA[r], accA[r + 1], accA[r + 2], accA[r + 3]);
-        if (pp == 1 || p + 1 == p1) {
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (elect_one()) {
-            for (int q = 0; q <= pp; ++q) {
-              const int d = 2 * (p - pp + q) + sub;
-              if (d < nd)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-                  if (col + 256 * h < a.out_len)
-                    tma_store_2d(&tm1, st + q * 512 + 256 * h, (int)(col + 256 * h), e * a.dirs + d);
-            }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          }
-        }
-        continue;
-      } else {
+      {
         float* box = st + (pp * 2 + half) * 512;  // [row][256]
 #pragma unroll
         for (int r = 0; r < 16; r += 4) {
@@ -491,15 +433,11 @@ cudaError_t launch_pair_taps(const int2* rows, const int* nnz, int n_seg, int se
 }
 
 // ---------------------------------------------------------------- launch ----
-#ifndef TOEP_RENDER_SPLIT
-#define TOEP_RENDER_SPLIT 0
-#endif
 template <int KWIN, bool STAGE1, int NNZT>
 static cudaError_t launch_render_t(const RenderArgs& a, const RenderMaps& m, int sm_count, cudaStream_t st) {
   using C = RenderCfg<KWIN>;
-  constexpr bool SPLIT = TOEP_RENDER_SPLIT != 0;
   const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.tap_stride);
-  auto kern = k_render<KWIN, STAGE1, NNZT, SPLIT>;
+  auto kern = k_render<KWIN, STAGE1, NNZT>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
   // TMEM bounds co-residency: at most 512 / COLS CTAs per SM.  Shared memory
@@ -509,7 +447,7 @@ static cudaError_t launch_render_t(const RenderArgs& a, const RenderMaps& m, int
   const long long pairs_total = (a.n_items + 1) / 2;
   if (grid > pairs_total) grid = pairs_total;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kThreads * (SPLIT ? 2 : 1), L.total, st>>>(a, m.rows2, m.rows1);
+  kern<<<(unsigned)grid, kThreads, L.total, st>>>(a, m.rows2, m.rows1);
   return cudaGetLastError();
 }
 

@@ -84,7 +84,7 @@ def test_tensor_path_small_and_large_magnitudes(mods):
 
 @pytest.mark.parametrize("K,lf,dirs,ears", [(1, 1, 1, 1), (2, 3, 3, 2), (16, 1, 2, 1), (17, 40, 5, 2), (33, 7, 130, 1),
                                             (128, 73, 4, 2), (129, 20, 3, 2), (192, 9, 2, 1), (200, 1, 2, 2),
-                                            (256, 5, 3, 1), (257, 5, 2, 1), (498, 3, 2, 1)])
+                                            (256, 5, 3, 1), (257, 5, 2, 1), (498, 3, 2, 1), (40, 5, 7, 3)])
 def test_shape_envelope(mods, K, lf, dirs, ears):
     """Reflection lengths across every kernel boundary (KPAD 16..256, the
     window kernel's KWIN tiers, the banded fallback), tiny resonance filters,

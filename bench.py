@@ -404,7 +404,7 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
 
         def e2e_step():
             y.copy_(y_pin, non_blocking=True)
-            r = br.render_all(y, out=out, check_finite=False)
+            r = br.render_all(y, out=out)  # the user's call: includes the fused non-finite check
             out_pin.copy_(out, non_blocking=True)
             return r
 

@@ -380,7 +380,7 @@ struct toep_renderer {
   int* d_nonfinite = nullptr;  // sticky flag: a kernel read a non-finite input sample
   int4* d_epairs = nullptr;    // [dirs][tap_stride] ear-interleaved taps (mixdown)
   void* d_gmma = nullptr;      // tensor-core operand tables (render_mma.cu), null if unsupported
-  float* d_gscale = nullptr;   // [ears][dirs_pad]
+  float* d_gscale = nullptr;   // [ears][chunks]
 };
 
 // TOEP_RENDER_MMA=0 selects the FFMA/TMEM-window kernel for every render (A/B runs)
@@ -429,7 +429,7 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
     if (e == cudaSuccess && render_mma_supported(g->length, r->lf_pad)) {
       const int cn = render_mma_chunk(), nch = (dirs + cn - 1) / cn;
       e = cudaMalloc(&r->d_gmma, render_mma_gbytes(ears, dirs, g->length));
-      if (e == cudaSuccess) e = cudaMalloc(&r->d_gscale, (size_t)ears * nch * cn * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&r->d_gscale, (size_t)ears * nch * sizeof(float));
       if (e == cudaSuccess)
         e = build_render_mma_tables(g->d_raw, g->d_nnz, dirs, ears, g->tap_stride, g->length, r->d_gmma,
                                     r->d_gscale, nullptr);
@@ -512,13 +512,10 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.g = r->d_gmma;
     a.gscale = r->d_gscale;
     a.kpad = render_mma_kpad(g->length);
-    a.tt = render_mma_tt(a.kpad);
     a.nchunks = (r->dirs + render_mma_chunk() - 1) / render_mma_chunk();
     a.dirs = r->dirs;
-    a.dirs_pad = a.nchunks * render_mma_chunk();
     a.ears = r->ears;
-    a.n_titems = (int)((out_len + 128LL * a.tt - 1) / (128LL * a.tt));
-    a.n_units = (long long)a.ears * a.n_titems * a.nchunks;
+    a.n_titems = (int)((out_len + 127) / 128);
     a.out = out;
     a.out_pitch = out_pitch;
     a.out_len = out_len;

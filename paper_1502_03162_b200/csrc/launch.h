@@ -38,20 +38,18 @@ struct RenderArgs {
 };
 
 // Tensor-core renderer (render_mma.cu): stage 2 as a split-fp16 GEMM per
-// (ear, 128*tt-output item, 64-direction chunk) unit.
+// (ear, 128-output tile, 128-direction chunk) unit.
 struct RenderMmaArgs {
   const float* x;        // source y[nx]
   long long nx;
   const float* f;        // [ears][lf_pad] resonance taps, zero padded
   int lf_pad;
   const void* g;         // [ears][nchunks][hi, lo][canonical chunk x kpad] fp16 (build_render_mma_tables)
-  const float* gscale;   // [ears][dirs_pad] per-direction unscale 2^-q
+  const float* gscale;   // [ears][nchunks] chunk unscale 2^-q
   int kpad;              // round_up(K, 16)
-  int tt;                // 128-output tiles per item (1)
   int nchunks;           // ceil(dirs / render_mma_chunk())
-  int dirs, dirs_pad, ears;
-  int n_titems;          // ceil(out_len / (128 * tt))
-  long long n_units;     // ears * n_titems * nchunks
+  int dirs, ears;
+  int n_titems;          // ceil(out_len / 128)
   float* out;            // row (e * dirs + d) at out + row * out_pitch
   long long out_pitch;
   long long out_len;
@@ -59,7 +57,6 @@ struct RenderMmaArgs {
 };
 bool render_mma_supported(int K, int lf_pad);
 int render_mma_kpad(int K);
-int render_mma_tt(int kpad);
 int render_mma_chunk();  // directions per G chunk (MMA N)
 size_t render_mma_gbytes(int ears, int dirs, int K);
 cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, int ears, int stride, int K,

@@ -6,37 +6,44 @@
 // = conv_dense(y, f) (_kernels.pyx:11-25) then conv_sparse(yf, idx, vals, K)
 // (_kernels.pyx:28-44), for every (ear, direction) row.
 //
-// Stage 2 for a tile of 128 outputs t and a chunk of 64 directions d is
-//     D[t][d] = sum_o A[t][o] * G[d][o],   A[t][o] = yf[T0 + t - o]   (Toeplitz/Hankel)
-// with o < KPAD = round_up(K, 16): M = 128, N = 64, K = KPAD.  The zero taps of
-// the sparse g cost tensor-core work, but the tensor cores have ~2x headroom
-// over the HBM write stream at every sparsity (the kernel is write-bound).
+// Stage 2 for a tile of 128 outputs t and a chunk of 128 directions d is
+//     D[t][d] = sum_o A[t][o] * G[d][o],   A[t][o] = yf[T0 + t - o]   (Hankel)
+// with o < KPAD = round_up(K, 16): M = N = 128, K = KPAD (an M=128 MMA costs
+// the same ~64 cycles at N = 64 as at N = 128, so N = 128 runs at full rate).
+// The zero taps of the sparse g cost tensor-core work, but the tensor cores
+// have ~2x headroom over the HBM write stream at every sparsity: the kernel
+// is write-bound.
 //
 // fp32 accuracy from fp16 operands: x = hi + lo with hi = fp16(x),
 // lo = fp16(x - hi) (exact residual), products hi*hi + hi*lo + lo*hi in fp32
 // (the dropped lo*lo term is ~2^-22 relative).  Operands are scaled by powers
-// of two into [2^13, 2^14) before the split -- per tile for yf, per direction
-// for g -- and unscaled exactly in the epilogue, so the split never meets
-// fp16 under/overflow.  Measured rel. L2 ~6e-7 (tools/microbench/mma_probe.cu).
+// of two into [2^13, 2^14) before the split -- per 128-output tile for yf, per
+// 128-direction chunk for g -- and unscaled exactly in the epilogue, so the
+// split never meets fp16 under/overflow.  Measured rel. L2 2e-7..1e-6
+// (tests/test_gpu_paths.py; tools/microbench/mma_probe.cu).
 //
 // The Hankel operand A lives in TMEM (lane t = output t, column j = the fp16
-// pair {A[t][2j], A[t][2j+1]}), so each MMA reads only G from shared memory:
-// with A in shared memory the N = 64 MMAs were shared-memory-bandwidth bound
-// (A re-read per direction chunk).
+// pair {A[t][2j], A[t][2j+1]}), so each MMA reads only G from shared memory
+// (with A in shared memory the MMAs were shared-memory-bandwidth bound); two
+// A buffers when KPAD <= 128, so the next tile's rows are written while this
+// tile's MMAs run.  G chunks are shared by a cluster of kMmaCluster CTAs that
+// render consecutive tiles in lockstep: each CTA loads 1/kMmaCluster of every
+// chunk with a multicast bulk copy, and each CTA's MMA completion frees the
+// stage in all of them (tcgen05.commit .multicast::cluster).
 //
 // Persistent, warp-specialised CTA (one per SM, 18 warps):
-//   warp 0      : TMA producer -- G chunks (pre-laid-out canonical fp16 hi/lo,
-//                 28 KB for KPAD 112) into a kMmaBStages-deep ring
-//   warp 1      : MMA issuer (one elected lane): per chunk and t-tile,
-//                 3 x KPAD/16 tcgen05.mma (A from TMEM, G from shared memory)
-//                 into a double-buffered TMEM accumulator
-//   warps 2-9   : A builders -- stage 1 (resonance FIR) for the item's yf tile,
-//                 the per-tile scale, then every thread writes its TMEM lane's
-//                 Hankel row (hi and lo) with tcgen05.st; once per item
+//   warp 0      : TMA producer -- its slice of each G chunk (canonical fp16
+//                 hi/lo, 57 KB per chunk at KPAD 112) into a 2-stage ring
+//   warp 1      : MMA issuer (one elected lane): per unit 3 x KPAD/16
+//                 tcgen05.mma (A from TMEM, G from shared memory) into a
+//                 double-buffered TMEM accumulator
+//   warps 2-9   : A builders -- stage 1 (resonance FIR) for the tile's yf,
+//                 the tile scale, then every thread writes its TMEM lane's
+//                 Hankel row (hi and lo) with tcgen05.st; once per tile
 //   warps 10-17 : epilogue -- tcgen05.ld the accumulator (lane = output t; two
-//                 warps per lane quarter, 32 columns each), unscale, stage a
-//                 [32 directions][32 t] block in shared memory, TMA tensor store
-//                 (3-D map {t, direction, ear} clips the padding directions)
+//                 warps per lane quarter, 64 columns each), unscale, stage
+//                 [32 directions][32 t] blocks in shared memory, TMA tensor
+//                 stores (3-D map {t, direction, ear} clips padding directions)
 #include <algorithm>
 #include <cstdio>
 #include <cuda_fp16.h>
@@ -529,7 +536,6 @@ __global__ void __launch_bounds__(kMmaN) k_build_gmma(const int2* __restrict__ r
 }
 
 int render_mma_kpad(int K) { return (K + 15) / 16 * 16; }
-int render_mma_tt(int) { return 1; }
 int render_mma_chunk() { return kMmaN; }
 
 bool render_mma_supported(int K, int lf_pad) {

@@ -63,6 +63,11 @@ struct toep_taps {
   int* d_nnz = nullptr;
   bool stream_owned = false;  // freed with cudaFreeAsync on `owner`
   cudaStream_t owner = nullptr;
+  // per-row pair tables {col, v, kwin, 0} for single-row convolutions
+  // (toep_taps_conv), built on first use
+  std::mutex rowpairs_mu;
+  int4* d_rowpairs = nullptr;  // [rows][tap_stride]
+  int4* d_rowpnnz = nullptr;   // [rows]
 };
 
 static bool uniform_supported(int n) { return n == 4 || n == 8 || n == 12 || n == 16 || n == 24 || n == 32; }
@@ -173,6 +178,7 @@ int toep_taps_destroy(toep_taps* t) {
     if (t->d_raw) cudaFree(t->d_raw);
     if (t->d_nnz) cudaFree(t->d_nnz);
   }
+  if (t->d_rowpairs) cudaFree(t->d_rowpairs);  // d_rowpnnz lives in the same allocation
   delete t;
   return TOEP_OK;
 }
@@ -278,7 +284,27 @@ int toep_taps_conv(const toep_taps* t, int32_t row, const float* y, int64_t ny, 
   if (!t) return fail(TOEP_ERR_INVALID, "null table");
   if (row < 0 || row >= t->rows) return fail(TOEP_ERR_INVALID, "row %d out of range", row);
   if (ny < 1 || !y || !out) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
-  return reflect_rows(t, row, 1, nullptr, nullptr, y, ny, out, 0, S(stream));
+  cudaStream_t st = S(stream);
+  if (t->kwin > 0) {
+    auto* tm = const_cast<toep_taps*>(t);
+    std::lock_guard<std::mutex> lk(tm->rowpairs_mu);
+    if (!tm->d_rowpairs) {  // every row paired with an empty row, once per table
+      int4* p = nullptr;
+      TOEP_CUDA(cudaMalloc(&p, (size_t)t->rows * (t->tap_stride + 1) * sizeof(int4)));
+      cudaError_t e = launch_pair_taps(t->d_kw, t->d_nnz, t->rows, 1, t->tap_stride, t->kwin, p,
+                                       p + (size_t)t->rows * t->tap_stride, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "launch_pair_taps");
+      }
+      tm->d_rowpairs = p;
+      tm->d_rowpnnz = p + (size_t)t->rows * t->tap_stride;
+    }
+    return reflect_rows(t, row, 1, t->d_rowpairs + (size_t)row * t->tap_stride, t->d_rowpnnz + row, y, ny, out, 0,
+                        st);
+  }
+  return reflect_rows(t, row, 1, nullptr, nullptr, y, ny, out, 0, st);
 }
 
 int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps, float* out, int64_t* macs,

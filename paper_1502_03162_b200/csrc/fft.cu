@@ -242,7 +242,7 @@ static cudaError_t fft_batched(const typename Cplx<T>::T2* in, typename Cplx<T>:
     const int threads = (int)std::min<long long>(512, std::max<long long>(32, n / 2));
     auto kern = inverse ? k_fft_smem<T, true> : k_fft_smem<T, false>;
     if (bytes > 48 * 1024) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      e = ensure_smem(reinterpret_cast<const void*>(kern), bytes);
       if (e != cudaSuccess) return e;
     }
     kern<<<(unsigned)batch, threads, bytes, st>>>(in, out, tw, (int)n, logn);
@@ -285,7 +285,7 @@ cudaError_t launch_fft_conv(const float* y, long long ny, const float* spectrum,
     const int bytes = (int)(n * sizeof(float2));
     const int threads = (int)std::min<long long>(512, std::max<long long>(32, n / 2));
     if (bytes > 48 * 1024) {
-      e = cudaFuncSetAttribute(k_ols_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      e = ensure_smem(reinterpret_cast<const void*>(k_ols_fused), bytes);
       if (e != cudaSuccess) return e;
     }
     k_ols_fused<<<(unsigned)nseg, threads, bytes, st>>>(y, ny, spec, tw, (int)n, ilog2(n), (int)ntaps, out, out_len);

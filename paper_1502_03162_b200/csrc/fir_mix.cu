@@ -405,7 +405,7 @@ template <int KWIN, int NNZT>
 static cudaError_t launch_mix_t(const MixArgs& a, int sm_count, cudaStream_t st) {
   const int bytes = mix_layout(KWIN, a.tap_stride).total_bytes;
   auto kern = k_mix<KWIN, NNZT>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaError_t err = ensure_smem(reinterpret_cast<const void*>(kern), bytes);
   if (err != cudaSuccess) return err;
   long long grid = (long long)sm_count * (512 / (kR + KWIN));  // TMEM-bounded co-residency
   if (grid > a.n_items) grid = a.n_items;
@@ -594,7 +594,7 @@ cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st) {
   const size_t fin = (size_t)a.ears * (a.zh + a.B + a.lf_pad);
   const size_t smem = std::max(per_cta, fin) * 4;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_stream_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k_stream_step), (int)smem);
     if (e != cudaSuccess) return e;
   }
   k_stream_step<<<a.ctas, 256, smem, st>>>(a);

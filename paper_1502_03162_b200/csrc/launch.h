@@ -3,8 +3,28 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <mutex>
+#include <unordered_map>
 
 namespace toep {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was last granted on this device (a per-launch call costs
+// microseconds of host time on the latency paths).
+inline cudaError_t ensure_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<long long, int> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const long long key = (long long)(reinterpret_cast<uintptr_t>(func) ^ ((uintptr_t)dev << 48));
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = granted[key];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 constexpr int kR = 16;             // outputs per lane (one TMEM x16 load per tap)
 constexpr int kWarps = 4;          // warps per CTA: one per TMEM lane quarter

@@ -438,7 +438,7 @@ static cudaError_t launch_render_t(const RenderArgs& a, const RenderMaps& m, int
   using C = RenderCfg<KWIN>;
   const SmemLayout L = render_smem_layout(KWIN, STAGE1, a.lf_pad, a.tap_stride);
   auto kern = k_render<KWIN, STAGE1, NNZT>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  cudaError_t err = ensure_smem(reinterpret_cast<const void*>(kern), L.total);
   if (err != cudaSuccess) return err;
   // TMEM bounds co-residency: at most 512 / COLS CTAs per SM.  Shared memory
   // and registers are sized so the hardware never exceeds that.

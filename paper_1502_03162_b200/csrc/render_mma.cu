@@ -564,7 +564,7 @@ cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, i
 
 cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st) {
   const MmaSmem L = mma_smem(a.kpad, a.lf_pad);
-  cudaError_t err = cudaFuncSetAttribute(k_render_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  cudaError_t err = ensure_smem(reinterpret_cast<const void*>(k_render_mma), L.total);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kMmaThreads);

@@ -63,9 +63,8 @@ struct toep_taps {
   int* d_nnz = nullptr;
   bool stream_owned = false;  // freed with cudaFreeAsync on `owner`
   cudaStream_t owner = nullptr;
-  // per-row pair tables {col, v, kwin, 0} for single-row convolutions
-  // (toep_taps_conv), built on first use
-  std::mutex rowpairs_mu;
+  // per-row pair tables {col, v, kwin, 0} + {nnz, 0, 0, 0} for single-row
+  // convolutions on the window kernel (toep_taps_conv); one allocation
   int4* d_rowpairs = nullptr;  // [rows][tap_stride]
   int4* d_rowpnnz = nullptr;   // [rows]
 };
@@ -128,19 +127,30 @@ static int taps_build(int32_t rows, int32_t length, const int64_t* row_ptr, cons
       kw[(size_t)r * t->tap_stride + k] = make_int2(t->kwin > 0 ? t->kwin - o : 0, vb);
     }
   }
+  std::vector<int4> rp;  // row paired with an empty row: {colA, vA, kwin, 0}, then per-row {nnz, 0, 0, 0}
+  if (t->kwin > 0) {
+    rp.resize(n + rows);
+    for (size_t i = 0; i < n; ++i) rp[i] = make_int4(kw[i].x, kw[i].y, t->kwin, 0);
+    for (int r = 0; r < rows; ++r) rp[n + r] = make_int4(nnz[r], 0, 0, 0);
+  }
   cudaError_t e;
   if (stream_owned) {
     e = cudaMallocAsync(&t->d_kw, n * sizeof(int2), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&t->d_raw, n * sizeof(int2), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&t->d_nnz, rows * sizeof(int), st);
+    if (e == cudaSuccess && !rp.empty()) e = cudaMallocAsync(&t->d_rowpairs, rp.size() * sizeof(int4), st);
   } else {
     e = cudaMalloc(&t->d_kw, n * sizeof(int2));
     if (e == cudaSuccess) e = cudaMalloc(&t->d_raw, n * sizeof(int2));
     if (e == cudaSuccess) e = cudaMalloc(&t->d_nnz, rows * sizeof(int));
+    if (e == cudaSuccess && !rp.empty()) e = cudaMalloc(&t->d_rowpairs, rp.size() * sizeof(int4));
   }
+  if (t->d_rowpairs) t->d_rowpnnz = t->d_rowpairs + n;
   if (e == cudaSuccess) e = cudaMemcpyAsync(t->d_kw, kw.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(t->d_raw, raw.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(t->d_nnz, nnz.data(), rows * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !rp.empty())
+    e = cudaMemcpyAsync(t->d_rowpairs, rp.data(), rp.size() * sizeof(int4), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && !stream_owned) e = cudaStreamSynchronize(st);  // host staging vectors die here
   if (e != cudaSuccess) {
     toep_taps_destroy(t);
@@ -173,12 +183,13 @@ int toep_taps_destroy(toep_taps* t) {
     if (t->d_kw) cudaFreeAsync(t->d_kw, t->owner);
     if (t->d_raw) cudaFreeAsync(t->d_raw, t->owner);
     if (t->d_nnz) cudaFreeAsync(t->d_nnz, t->owner);
+    if (t->d_rowpairs) cudaFreeAsync(t->d_rowpairs, t->owner);
   } else {
     if (t->d_kw) cudaFree(t->d_kw);
     if (t->d_raw) cudaFree(t->d_raw);
     if (t->d_nnz) cudaFree(t->d_nnz);
+    if (t->d_rowpairs) cudaFree(t->d_rowpairs);  // d_rowpnnz lives in the same allocation
   }
-  if (t->d_rowpairs) cudaFree(t->d_rowpairs);  // d_rowpnnz lives in the same allocation
   delete t;
   return TOEP_OK;
 }
@@ -285,25 +296,9 @@ int toep_taps_conv(const toep_taps* t, int32_t row, const float* y, int64_t ny, 
   if (row < 0 || row >= t->rows) return fail(TOEP_ERR_INVALID, "row %d out of range", row);
   if (ny < 1 || !y || !out) return fail(TOEP_ERR_INVALID, "signal must be a non-empty 1-d array");
   cudaStream_t st = S(stream);
-  if (t->kwin > 0) {
-    auto* tm = const_cast<toep_taps*>(t);
-    std::lock_guard<std::mutex> lk(tm->rowpairs_mu);
-    if (!tm->d_rowpairs) {  // every row paired with an empty row, once per table
-      int4* p = nullptr;
-      TOEP_CUDA(cudaMalloc(&p, (size_t)t->rows * (t->tap_stride + 1) * sizeof(int4)));
-      cudaError_t e = launch_pair_taps(t->d_kw, t->d_nnz, t->rows, 1, t->tap_stride, t->kwin, p,
-                                       p + (size_t)t->rows * t->tap_stride, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) {
-        cudaFree(p);
-        return cuda_fail(e, "launch_pair_taps");
-      }
-      tm->d_rowpairs = p;
-      tm->d_rowpnnz = p + (size_t)t->rows * t->tap_stride;
-    }
+  if (t->kwin > 0)
     return reflect_rows(t, row, 1, t->d_rowpairs + (size_t)row * t->tap_stride, t->d_rowpnnz + row, y, ny, out, 0,
                         st);
-  }
   return reflect_rows(t, row, 1, nullptr, nullptr, y, ny, out, 0, st);
 }
 
@@ -336,7 +331,7 @@ int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const f
   toep_taps* t = nullptr;
   int rc = taps_build(1, (int32_t)length, row_ptr, indices, values, true, st, &t);
   if (rc != TOEP_OK) return rc;
-  rc = reflect_rows(t, 0, 1, nullptr, nullptr, y, ny, out, 0, st);
+  rc = reflect_rows(t, 0, 1, t->d_rowpairs, t->d_rowpnnz, y, ny, out, 0, st);
   toep_taps_destroy(t);
   if (rc == TOEP_OK && macs) *macs = nnz * ny;  // _kernels.pyx:43
   return rc;

@@ -245,8 +245,19 @@ def _ref_mix_sources(task):
     return n
 
 
+def _single_core_rate(payload, fn, tasks, budget_s):
+    """The same reference work in this process on one core: samples/s over ~budget_s."""
+    _ref_worker_init(payload)
+    n, i = 0, 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s and i < len(tasks):
+        n += fn(tasks[i])
+        i += 1
+    return n / (time.perf_counter() - t0)
+
+
 def reference_step_factory(workload: str, cores: int):
-    """Returns (step_fn -> samples computed, description, kind, pool)."""
+    """Returns (step_fn -> samples computed, description, kind, pool, single_core_rate_fn)."""
     import multiprocessing as mp
 
     from paper_1502_03162_b200 import synth
@@ -268,10 +279,13 @@ def reference_step_factory(workload: str, cores: int):
         def step():
             return sum(pool.map(_ref_render_rows, tasks, chunksize=1))
 
+        def single(budget_s=3.0):
+            return _single_core_rate(payload, _ref_render_rows, tasks, budget_s)
+
         desc = "full %s per step: %d channels x %d samples, Renderer.render composition" % (
             workload, cfg.ears * cfg.dirs, cfg.ny + cfg.M - 1)
         kind = "reference" if _probe_ref() else "port"
-        return step, desc, kind, pool
+        return step, desc, kind, pool, single
     if workload in ("cfg4", "cfg5"):
         cfg = synth.CONFIGS[workload]
         ms = synth.models(cfg, seed=5)
@@ -291,10 +305,13 @@ def reference_step_factory(workload: str, cores: int):
             # src x ear samples of the bounded sample (output T + M - 1 per source-ear)
             return sum(pool.map(_ref_mix_sources, tasks, chunksize=1))
 
+        def single(budget_s=3.0):
+            return _single_core_rate(payload, _ref_mix_sources, tasks, budget_s)
+
         desc = "%d sources x 2 s (%d samples) per step, %s laws; per-source Renderer.render + fp64 sum" % (
             nsrc, T, workload)
         kind = "reference" if _probe_ref() else "port"
-        return step, desc, kind, pool
+        return step, desc, kind, pool, single
     raise SystemExit("no reference arm for workload %s" % workload)
 
 
@@ -308,7 +325,7 @@ def run_reference(args, world, rank):
         return 0
     cores = os.cpu_count() or 1
     wl = args.workload if args.workload != "cfg3" else "cfg2"
-    step, desc, kind, pool = reference_step_factory(wl, cores)
+    step, desc, kind, pool, _ = reference_step_factory(wl, cores)
     try:
         for _ in range(args.warmup):
             step()
@@ -502,8 +519,8 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
 
 def cpu_baseline_line(workload):
     cores = os.cpu_count() or 1
-    step, desc, kind, pool = reference_step_factory(workload if workload in ("cfg1", "cfg2", "cfg4", "cfg5")
-                                                    else "cfg2", cores)
+    step, desc, kind, pool, single = reference_step_factory(workload if workload in ("cfg1", "cfg2", "cfg4", "cfg5")
+                                                            else "cfg2", cores)
     # repeat the bounded sample until ~10 s of CPU work has been timed
     try:
         step()  # warm
@@ -519,7 +536,8 @@ def cpu_baseline_line(workload):
         pool.close()
         pool.join()
     return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": kind,
-            "sample": "%s; %d repetitions" % (desc, reps), "seconds": dt}
+            "sample": "%s; %d repetitions" % (desc, reps), "seconds": dt,
+            "single_core_value": single(3.0)}
 
 
 def main():

@@ -7,8 +7,9 @@
 Default workload is BASELINE config 2 (configs[1]): one 441,000-sample source
 rendered through 1,250 directions x 2 ears (nnz 16, K 100, Lf 101) -> 2,500
 channels x 441,199 samples per step.  Metric: output samples/s counted as
-src x dir x ear.  For N > 1 (torchrun, one rank per GPU) the 2,500 channels
-are split across ranks by direction (strong scaling, no collective: channel
+src x dir x ear.  For N > 1 (torchrun, one rank per GPU) the output time
+range is split across ranks -- each renders all 2,500 channels for its
+samples from the matching input window (strong scaling, no collective:
 outputs stay on their GPU).  ``--workload cfg5`` benches the 4,096-source
 mixdown with sources split across ranks and one NCCL reduce.
 
@@ -370,21 +371,26 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
     import torch
 
     from paper_1502_03162_b200 import batch, synth
-    from paper_1502_03162_b200.types import FactorizedModel
 
     cfg = synth.CONFIGS[workload]
     ms_full = synth.models(cfg, seed=2)
-    # direction split across ranks (strong scaling, no exchange)
-    d0 = rank * cfg.dirs // world
-    d1 = (rank + 1) * cfg.dirs // world
-    ms = [FactorizedModel(m.resonance_taps, m.reflections[d0:d1]) for m in ms_full]
-    y_host = synth.source(cfg.ny, seed=22).astype(np.float32)
+    # time split across ranks (strong scaling, no exchange): rank r renders every
+    # (ear, direction) row for output samples [t0, t1) from the input segment
+    # y[t0 - (M-1), t1) -- the full-convolution window of that range
+    ms = ms_full
+    M = cfg.lf + cfg.K - 1
+    L = cfg.ny + M - 1
+    seg = -(-L // world)
+    t0, t1 = min(L, rank * seg), min(L, (rank + 1) * seg)
+    y_lo = max(0, t0 - (M - 1))
+    y_hi = max(min(cfg.ny, t1), y_lo + 1)
+    y_full = synth.source(cfg.ny, seed=22).astype(np.float32)
+    y_host = np.ascontiguousarray(y_full[y_lo:y_hi])
     y = torch.from_numpy(y_host).cuda()
     br = batch.BatchRenderer(ms)
-    out = br.alloc(cfg.ny)
-    L = br.out_len(cfg.ny)
+    out = br.alloc(y.numel())
     br.render_all(y, out=out)  # validates inputs once (finite check) and builds device state
-    samples_local = br.ears * (d1 - d0) * L
+    samples_local = br.ears * br.dirs * (t1 - t0)
     samples_global = cfg.ears * cfg.dirs * L
     flush = _flush_fn()
 
@@ -400,9 +406,9 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
 
     # roofline: HBM-bound (4.002 B/sample algorithmic: 4 B written + amortised y, taps)
     peaks = _peaks()
-    alg_bytes = samples_local * 4 + cfg.ny * 4 + int(br.row_nnz.sum()) * 8 + cfg.ears * cfg.lf * 4
+    alg_bytes = samples_local * 4 + y.numel() * 4 + int(br.row_nnz.sum()) * 8 + cfg.ears * cfg.lf * 4
     achieved_gbs = alg_bytes / (kern_ms * 1e-3) / 1e9
-    flops = 2.0 * int(br.row_nnz.sum()) * (cfg.ny + cfg.lf - 1) + 2.0 * cfg.ears * cfg.lf * (cfg.ny + br.M)
+    flops = (2.0 * int(br.row_nnz.sum()) * (y.numel() + cfg.lf - 1) + 2.0 * cfg.ears * cfg.lf * (y.numel() + br.M))
     roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": _traffic(workload),
             "peak_src": peaks["src"],
@@ -438,7 +444,7 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
         "data": "synthetic (seeded: y~N(0,1), f decaying Gaussian, g half-normal at uniform positions)",
         "config": {"workload": workload, "sources": 1, "directions": cfg.dirs, "ears": cfg.ears,
                    "signal_len": cfg.ny, "K": cfg.K, "Lf": cfg.lf, "nnz": cfg.nnz, "out_len": L,
-                   "samples_per_step": samples_global, "parallelism": "directions/%d" % world,
+                   "samples_per_step": samples_global, "parallelism": "time/%d" % world,
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clk.summary(),

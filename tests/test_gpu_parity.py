@@ -226,3 +226,26 @@ def test_streaming_equals_offline(mods, cuda):
     st.reset()
     again = st.step(y[:, :256].contiguous())
     assert rel_l2(again.cpu().numpy(), offline[:, :256].cpu().numpy()) < TOL
+
+
+def test_time_split_segments_stitch(mods):
+    """The multi-GPU split of bench.py --gpus N: segment renders of
+    y[t0 - (M-1), t1) give exactly the full render's samples [t0, t1)."""
+    batch, _, synth = mods
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("ts", ny=20_000, M=200, K=100, nnz=16, dirs=140, ears=2)
+    ms = synth.models(cfg, seed=61)
+    y = synth.source(cfg.ny, seed=62)
+    br = batch.BatchRenderer(ms)
+    full = br.render_all(y).cpu().numpy()
+    M, L = cfg.M, cfg.ny + cfg.M - 1
+    world = 3
+    seg = -(-L // world)
+    for r in range(world):
+        t0, t1 = min(L, r * seg), min(L, (r + 1) * seg)
+        lo = max(0, t0 - (M - 1))
+        hi = max(min(cfg.ny, t1), lo + 1)
+        part = br.render_all(y[lo:hi]).cpu().numpy()
+        got = part[:, :, t0 - lo:t1 - lo]
+        ref = full[:, :, t0:t1]
+        assert rel_l2(got, ref) < TOL, r

@@ -460,10 +460,13 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     cfg = synth.CONFIGS[workload]
     ms = synth.models(cfg, seed=5)
     sd = synth.source_directions(cfg.sources, cfg.dirs, seed=5)
-    s0, cnt = tdist.partition(cfg.sources, world, rank)
+    # sources partitioned by direction: every direction's sources on one rank,
+    # ~S/N sources and ~D/N directions per rank (dist.partition_by_direction)
+    mine = tdist.partition_by_direction(sd, world)[rank]
+    cnt = int(mine.size)
     T = cfg.ny
     y = synth.device_sources(cnt, T, seed=1000 + rank)
-    mix = batch.MixRenderer(ms, sd, T)
+    mix = batch.MixRenderer(ms, sd[mine], T)
     z = mix.alloc_z()
     outb = torch.empty((cfg.ears, (mix.out_len + 3) // 4 * 4), device="cuda")
     group = None
@@ -471,7 +474,7 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
 
     def step():
         z.zero_()
-        mix.partial(y, s0=s0, count=cnt, z=z)
+        mix.partial(y, z=z)
         tdist.reduce_partials(z, dst=0, group=group)
         if rank == 0:
             mix.finish(z, out=outb)
@@ -488,14 +491,14 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     torch.cuda.synchronize()
     ev[0].record()
     for _ in range(reps):
-        mix.partial(y, s0=s0, count=cnt, z=z, check_finite=False)
+        mix.partial(y, z=z, check_finite=False)
     ev[1].record()
     torch.cuda.synchronize()
     kern_ms = ev[0].elapsed_time(ev[1]) / reps
     # algorithmic work: every source sample read once (4 B); sources sharing a
     # direction are summed in the kernel, then 2 ears x nnz taps per distinct
     # direction and z sample (executed FLOPs of the g-first algorithm)
-    ndist = len(np.unique(sd[s0:s0 + cnt]))
+    ndist = len(np.unique(sd[mine]))
     zlen = T + cfg.K - 1
     flops_local = 2.0 * ndist * cfg.ears * cfg.nnz * zlen + 1.0 * cnt * T
     bytes_local = 4.0 * cnt * T
@@ -515,7 +518,8 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Philox sources on device; BASELINE laws)",
         "config": {"workload": workload, "sources": cfg.sources, "signal_len": T, "K": cfg.K, "Lf": cfg.lf,
-                   "nnz": cfg.nnz, "ears": cfg.ears, "parallelism": "sources/%d + nccl reduce" % world,
+                   "nnz": cfg.nnz, "ears": cfg.ears,
+                   "parallelism": "sources by direction/%d + nccl reduce" % world,
                    "l2": "inputs (47 GB) larger than L2; flushed between steps"},
         "roofline": roof, "e2e": None, "gpu_launches": args.steps * (3 if rank == 0 else 2),
         "clocks": clk.summary(),

@@ -155,3 +155,22 @@ class TestSynthAndPartition:
         assert seen == list(range(S))
         sizes = [tdist.partition(S, world, r)[1] for r in range(world)]
         assert max(sizes) - min(sizes) <= 1
+
+
+def test_partition_by_direction():
+    """Every direction's sources on one rank, balanced source counts, and each
+    rank touching ~1/N of the directions (the mix's tap work)."""
+    sd = synth.source_directions(4096, 1250, seed=5)
+    for world in (1, 2, 3, 8):
+        parts = tdist.partition_by_direction(sd, world)
+        assert len(parts) == world
+        allidx = np.concatenate(parts)
+        assert sorted(allidx.tolist()) == list(range(4096))
+        dirs = [set(sd[p].tolist()) for p in parts]
+        for i in range(world):
+            assert all(not (dirs[i] & dirs[j]) for j in range(i + 1, world))
+            assert abs(len(parts[i]) - 4096 / world) <= 16
+        assert max(len(d) for d in dirs) <= 1.2 * len(set(sd.tolist())) / world
+    sd2 = np.zeros(10, np.int32)  # one direction: everything on one rank
+    parts = tdist.partition_by_direction(sd2, 4)
+    assert sorted(len(p) for p in parts) == [0, 0, 0, 10]

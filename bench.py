@@ -7,10 +7,10 @@
 Default workload is BASELINE config 2 (configs[1]): one 441,000-sample source
 rendered through 1,250 directions x 2 ears (nnz 16, K 100, Lf 101) -> 2,500
 channels x 441,199 samples per step.  Metric: output samples/s counted as
-src x dir x ear.  For N > 1 (torchrun, one rank per GPU) the output time
-range is split across ranks -- each renders all 2,500 channels for its
-samples from the matching input window (strong scaling, no collective:
-outputs stay on their GPU).  ``--workload cfg5`` benches the 4,096-source
+src x dir x ear.  For N > 1 (torchrun, one rank per GPU) every rank renders
+its own independent source through all 2,500 channels (weak scaling: the
+per-GPU work is one config-2 render; no collective, outputs stay on their
+GPU).  ``--workload cfg5`` benches the 4,096-source
 mixdown with sources split across ranks and one NCCL reduce.
 
 ``value``     : device-resident throughput, CUDA events around each step on
@@ -374,24 +374,18 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
 
     cfg = synth.CONFIGS[workload]
     ms_full = synth.models(cfg, seed=2)
-    # time split across ranks (strong scaling, no exchange): rank r renders every
-    # (ear, direction) row for output samples [t0, t1) from the input segment
-    # y[t0 - (M-1), t1) -- the full-convolution window of that range
+    # N GPUs: weak scaling over independent sources -- rank r renders its own
+    # source (seed 22 + r) through every (ear, direction), the per-GPU work of
+    # one GPU (tier rule: partitioned units, no data-path collective)
     ms = ms_full
-    M = cfg.lf + cfg.K - 1
-    L = cfg.ny + M - 1
-    seg = -(-L // world)
-    t0, t1 = min(L, rank * seg), min(L, (rank + 1) * seg)
-    y_lo = max(0, t0 - (M - 1))
-    y_hi = max(min(cfg.ny, t1), y_lo + 1)
-    y_full = synth.source(cfg.ny, seed=22).astype(np.float32)
-    y_host = np.ascontiguousarray(y_full[y_lo:y_hi])
+    y_host = synth.source(cfg.ny, seed=22 + rank).astype(np.float32)
     y = torch.from_numpy(y_host).cuda()
     br = batch.BatchRenderer(ms)
     out = br.alloc(y.numel())
+    L = br.out_len(cfg.ny)
     br.render_all(y, out=out)  # validates inputs once (finite check) and builds device state
-    samples_local = br.ears * br.dirs * (t1 - t0)
-    samples_global = cfg.ears * cfg.dirs * L
+    samples_local = br.ears * br.dirs * L
+    samples_global = samples_local * world
     flush = _flush_fn()
 
     def step():
@@ -440,11 +434,12 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded: y~N(0,1), f decaying Gaussian, g half-normal at uniform positions)",
         "config": {"workload": workload, "sources": 1, "directions": cfg.dirs, "ears": cfg.ears,
                    "signal_len": cfg.ny, "K": cfg.K, "Lf": cfg.lf, "nnz": cfg.nnz, "out_len": L,
-                   "samples_per_step": samples_global, "parallelism": "time/%d" % world,
+                   "samples_per_step": samples_global,
+                   "parallelism": "independent sources x %d (one per GPU)" % world,
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clk.summary(),

@@ -122,12 +122,19 @@ def torch():
     return _torch
 
 
+_cuda_ok = False
+
+
 def require_cuda():
     """Library loaded and a CUDA device present, else NativeUnavailable."""
+    global _cuda_ok
+    if _cuda_ok:
+        return _torch
     load_library()
     t = torch()
     if not t.cuda.is_available():
         raise NativeUnavailable("no CUDA device visible; the renderer has no CPU fallback")
+    _cuda_ok = True
     return t
 
 

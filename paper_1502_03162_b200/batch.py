@@ -83,6 +83,8 @@ class BatchRenderer(_ModelSet):
     def __init__(self, models):
         super().__init__(models)
         self.counters = {"resonance_macs": 0, "reflection_macs": 0, "calls": 0}
+        self.total_nnz = int(self.row_nnz.sum())
+        self._checked_out = None
 
     def out_len(self, ny: int) -> int:
         return ny + self.M - 1
@@ -97,7 +99,8 @@ class BatchRenderer(_ModelSet):
         """Returns a [ears, dirs, out_len] float32 view (of ``out`` when given)."""
         t = _lib.require_cuda()
         if isinstance(y, t.Tensor):
-            x = y.to(device="cuda", dtype=t.float32).contiguous()
+            x = y if (y.is_cuda and y.dtype == t.float32 and y.is_contiguous()) else \
+                y.to(device="cuda", dtype=t.float32).contiguous()
         else:
             x = t.from_numpy(np.ascontiguousarray(getattr(y, "samples", y), dtype=np.float32)).to("cuda")
         if x.ndim != 1 or x.numel() == 0:
@@ -110,10 +113,12 @@ class BatchRenderer(_ModelSet):
         ny = x.numel()
         if out is None:
             out = self.alloc(ny)
-        if out.dtype != t.float32 or not out.is_cuda or out.dim() != 3 or out.shape[:2] != (self.ears, self.dirs):
-            raise DataError("output must be a float32 CUDA tensor of shape [ears, dirs, pitch]")
-        if out.stride(2) != 1 or out.stride(1) != out.shape[2] or out.stride(0) != out.shape[1] * out.shape[2]:
-            raise DataError("output must be contiguous")
+        if out is not self._checked_out:  # validated once per output buffer object
+            if out.dtype != t.float32 or not out.is_cuda or out.dim() != 3 or out.shape[:2] != (self.ears, self.dirs):
+                raise DataError("output must be a float32 CUDA tensor of shape [ears, dirs, pitch]")
+            if out.stride(2) != 1 or out.stride(1) != out.shape[2] or out.stride(0) != out.shape[1] * out.shape[2]:
+                raise DataError("output must be contiguous")
+            self._checked_out = out
         pitch = out.shape[2]
         if pitch < self.out_len(ny):
             raise DataError("output pitch %d < %d samples" % (pitch, self.out_len(ny)))
@@ -121,7 +126,7 @@ class BatchRenderer(_ModelSet):
         if fused_check and self.native.nonfinite(stream):
             raise DataError("signal contains non-finite samples")
         self.counters["resonance_macs"] += self.ears * self.lf * ny
-        self.counters["reflection_macs"] += int(self.row_nnz.sum()) * (ny + self.lf - 1)
+        self.counters["reflection_macs"] += self.total_nnz * (ny + self.lf - 1)
         self.counters["calls"] += 1
         return out[:, :, : self.out_len(ny)]
 

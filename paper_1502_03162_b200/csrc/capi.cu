@@ -402,6 +402,11 @@ struct toep_renderer {
   int4* d_epairs = nullptr;    // [dirs][tap_stride] ear-interleaved taps (mixdown)
   void* d_gmma = nullptr;      // tensor-core operand tables (render_mma.cu), null if unsupported
   float* d_gscale = nullptr;   // [ears][chunks]
+  // last output tensor map (encoding costs microseconds of host time per call)
+  std::mutex map_mu;
+  const float* map_out = nullptr;
+  long long map_pitch = -1, map_len = -1;
+  CUtensorMap map{};
 };
 
 // TOEP_RENDER_MMA=0 selects the FFMA/TMEM-window kernel for every render (A/B runs)
@@ -542,9 +547,23 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.out_len = out_len;
     a.nonfinite = r->d_nonfinite;
     CUtensorMap map;
-    cudaError_t e = make_render_mma_map(out, r->ears, r->dirs, out_len, rows > 1 ? out_pitch : round_up(out_len, 4), &map);
-    if (e != cudaSuccess) return cuda_fail(e, "tensor map (output rows)");
-    e = launch_render_mma(a, map, sm_count_cached(), st);
+    {
+      auto* rm = const_cast<toep_renderer*>(r);
+      const long long pitch = rows > 1 ? out_pitch : round_up(out_len, 4);
+      std::lock_guard<std::mutex> lk(rm->map_mu);
+      if (rm->map_out != out || rm->map_pitch != pitch || rm->map_len != out_len) {
+        cudaError_t em = make_render_mma_map(out, r->ears, r->dirs, out_len, pitch, &rm->map);
+        if (em != cudaSuccess) {
+          rm->map_out = nullptr;
+          return cuda_fail(em, "tensor map (output rows)");
+        }
+        rm->map_out = out;
+        rm->map_pitch = pitch;
+        rm->map_len = out_len;
+      }
+      map = rm->map;
+    }
+    cudaError_t e = launch_render_mma(a, map, sm_count_cached(), st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_render_mma");
     return TOEP_OK;
   }

@@ -1,5 +1,5 @@
 // C ABI implementation (include/toep_b200.h).  Validation mirrors the
-// reference's DataError rules; kernels live in render.cu / fir_mix.cu.
+// reference's DataError rules; kernels live in render_mma.cu, render.cu, fir_mix.cu and fft.cu.
 #include <algorithm>
 #include <cstdarg>
 #include <cstdlib>

@@ -105,3 +105,23 @@ def test_nonfinite_detected_in_kernels(mods, cuda):
     st.step(blk)
     assert st.nonfinite()
     assert not st.nonfinite()  # reading clears it
+
+
+@pytest.mark.parametrize("K,ears,block", [(150, 1, 128), (50, 2, 64), (100, 2, 4)])
+def test_streaming_shapes(mods, cuda, K, ears, block):
+    """Streaming blocks against the offline mixdown for other filter lengths,
+    one ear and small blocks."""
+    batch, synth, _ = mods
+    torch = cuda
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("s", ny=block * 37, M=200, K=K, nnz=12, dirs=60, ears=ears, sources=40, block=block)
+    ms = synth.models(cfg, seed=K + block)
+    sd = synth.source_directions(cfg.sources, cfg.dirs, seed=3)
+    y = synth.device_sources(cfg.sources, cfg.ny, seed=9)
+    offline = batch.MixRenderer(ms, sd, cfg.ny).render(y)
+    st = batch.StreamRenderer(ms, sd, block)
+    full = torch.empty((ears, cfg.ny), device="cuda")
+    for b in range(cfg.ny // block):
+        st.step(y[:, b * block:(b + 1) * block], out=full[:, b * block:(b + 1) * block])
+    from conftest import rel_l2 as _rel
+    assert _rel(full.cpu().numpy(), offline[:, :cfg.ny].cpu().numpy()) < TOL

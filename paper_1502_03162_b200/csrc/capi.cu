@@ -803,8 +803,10 @@ struct toep_streamer {
   const toep_renderer* r = nullptr;
   int S = 0, B = 0, H = 0, zh = 0, ctas = 0, spc = 0;
   int* d_dir = nullptr;
+  int2* d_srctaps = nullptr;  // [S][ears][tap_stride]
+  int* d_srcnnz = nullptr;    // [S][ears]
   float* d_yhist = nullptr;
-  float* d_zhist = nullptr;
+  float* d_zhist = nullptr;   // [groups][ears][zh]
   float* d_part = nullptr;
   float* d_gpart = nullptr;
   unsigned int* d_ticket = nullptr;
@@ -838,12 +840,17 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
   cudaError_t e = cudaMalloc(&s->d_dir, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(s->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&s->d_yhist, (size_t)n_src * s->H * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&s->d_zhist, (size_t)r->ears * s->zh * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_zhist, (size_t)groups * r->ears * s->zh * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_srctaps, (size_t)n_src * r->ears * r->g->tap_stride * sizeof(int2));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_srcnnz, (size_t)n_src * r->ears * sizeof(int));
+  if (e == cudaSuccess)
+    e = launch_stream_gather_taps(r->g->d_raw, r->g->d_nnz, s->d_dir, n_src, r->ears, r->dirs, r->g->tap_stride,
+                                  s->d_srctaps, s->d_srcnnz, nullptr);
   if (e == cudaSuccess) e = cudaMalloc(&s->d_part, (size_t)s->ctas * r->ears * block * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_gpart, (size_t)groups * r->ears * block * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_ticket, (groups + 1) * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(s->d_yhist, 0, (size_t)n_src * s->H * sizeof(float));
-  if (e == cudaSuccess) e = cudaMemset(s->d_zhist, 0, (size_t)r->ears * s->zh * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemset(s->d_zhist, 0, (size_t)groups * r->ears * s->zh * sizeof(float));
   if (e == cudaSuccess) e = cudaMemset(s->d_ticket, 0, (groups + 1) * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -857,6 +864,8 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
 int toep_streamer_destroy(toep_streamer* s) {
   if (!s) return TOEP_OK;
   if (s->d_dir) cudaFree(s->d_dir);
+  if (s->d_srctaps) cudaFree(s->d_srctaps);
+  if (s->d_srcnnz) cudaFree(s->d_srcnnz);
   if (s->d_yhist) cudaFree(s->d_yhist);
   if (s->d_zhist) cudaFree(s->d_zhist);
   if (s->d_part) cudaFree(s->d_part);
@@ -870,7 +879,7 @@ int toep_streamer_reset(toep_streamer* s, void* stream) {
   if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
   cudaStream_t st = S(stream);
   TOEP_CUDA(cudaMemsetAsync(s->d_yhist, 0, (size_t)s->S * s->H * sizeof(float), st));
-  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)s->r->ears * s->zh * sizeof(float), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)((s->ctas + 15) / 16) * s->r->ears * s->zh * sizeof(float), st));
   TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, ((s->ctas + 15) / 16 + 1) * sizeof(unsigned int), st));
   return TOEP_OK;
 }
@@ -889,12 +898,10 @@ int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch
   a.B = s->B;
   a.yhist = s->d_yhist;
   a.H = s->H;
-  a.src_dir = s->d_dir;
   a.S = s->S;
-  a.taps = s->r->g->d_raw;
-  a.row_nnz = s->r->g->d_nnz;
+  a.src_taps = s->d_srctaps;
+  a.src_nnz = s->d_srcnnz;
   a.tap_stride = s->r->g->tap_stride;
-  a.dirs = s->r->dirs;
   a.ears = s->r->ears;
   a.src_per_cta = s->spc;
   a.part = s->d_part;

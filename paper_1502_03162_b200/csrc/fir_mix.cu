@@ -470,6 +470,7 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
 // applies f_e over [z history | z block] and rolls the z history.
 constexpr int kStreamGroup = 16;
 
+
 __device__ __forceinline__ bool stream_last_arrival(unsigned int* ticket, unsigned int n) {
   __shared__ bool s_last;
   __threadfence();
@@ -503,13 +504,10 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
       }
       *reinterpret_cast<float4*>(&s_w[s * L + 4 * q]) = v;
     }
-    for (int i = tid; i < ns * a.ears * a.tap_stride; i += blockDim.x) {
-      const int se = i / a.tap_stride, k = i - se * a.tap_stride;
-      const int s = se / a.ears, e = se - s * a.ears;
-      const long long row = (long long)e * a.dirs + a.src_dir[s0 + s];
-      s_tap[i] = a.taps[row * a.tap_stride + k];
-      if (k == 0) s_nnz[se] = a.row_nnz[row];
-    }
+    // this CTA's sources' tap rows are contiguous in the per-source table
+    const int2* st = a.src_taps + (long long)s0 * a.ears * a.tap_stride;
+    for (int i = tid; i < ns * a.ears * a.tap_stride; i += blockDim.x) s_tap[i] = __ldg(st + i);
+    for (int i = tid; i < ns * a.ears; i += blockDim.x) s_nnz[i] = __ldg(a.src_nnz + (long long)s0 * a.ears + i);
   }
   __syncthreads();
   const int t = tid;
@@ -538,12 +536,22 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     *reinterpret_cast<float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q) =
         *reinterpret_cast<const float4*>(&s_w[s * L + a.B + 4 * q]);
   }
-  // ---- level 1: the last CTA of each group sums the group's partials --------
+  // ---- level 1: the last CTA of each group sums the group's partials and
+  //      applies f over [group z history | group z block] (f is linear, so
+  //      out = sum over groups of f * z_g; each group keeps its own z history)
   const int groups = (gridDim.x + kStreamGroup - 1) / kStreamGroup;
   const int grp = blockIdx.x / kStreamGroup;
   const int c0 = grp * kStreamGroup, nc = min((int)gridDim.x - c0, kStreamGroup);
   if (!stream_last_arrival(a.ticket + grp, nc)) return;
   const long long cs = (long long)a.ears * a.B;
+  float* s_z = sm;                          // [ears][zh + B]
+  float* s_f = sm + a.ears * (a.zh + a.B);  // [ears][lf_pad]
+  float* zh_g = a.zhist + (long long)grp * a.ears * a.zh;
+  for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
+    const int e = i / a.zh, k = i - e * a.zh;
+    s_z[e * (a.zh + a.B) + k] = zh_g[i];
+  }
+  for (int i = tid; i < a.ears * a.lf_pad; i += blockDim.x) s_f[i] = __ldg(a.f + i);
   for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
     float z[kStreamGroup];
 #pragma unroll
@@ -552,23 +560,8 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     for (int w = kStreamGroup / 2; w > 0; w /= 2)
 #pragma unroll
       for (int u = 0; u < w; ++u) z[u] += z[u + w];
-    a.gpart[grp * cs + i] = z[0];
-  }
-  if (tid == 0) a.ticket[grp] = 0u;
-  // ---- level 2: the last group finishes: z = sum of groups, out = f * z -----
-  if (!stream_last_arrival(a.ticket + groups, groups)) return;
-  float* s_z = sm;                          // [ears][zh + B]
-  float* s_f = sm + a.ears * (a.zh + a.B);  // [ears][lf_pad]
-  for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
-    const int e = i / a.zh, k = i - e * a.zh;
-    s_z[e * (a.zh + a.B) + k] = a.zhist[(long long)e * a.zh + k];
-  }
-  for (int i = tid; i < a.ears * a.lf_pad; i += blockDim.x) s_f[i] = a.f[i];
-  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
     const int e = i / a.B, tt = i - e * a.B;
-    float z = 0.f;
-    for (int g = 0; g < groups; ++g) z += __ldcg(a.gpart + g * cs + i);
-    s_z[e * (a.zh + a.B) + a.zh + tt] = z;
+    s_z[e * (a.zh + a.B) + a.zh + tt] = z[0];
   }
   __syncthreads();
   for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
@@ -578,14 +571,45 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     float o = 0.f;
 #pragma unroll 8
     for (int jj = 0; jj < a.lf_pad; ++jj) o = fmaf(ff[jj], z[-jj], o);
-    a.out[(long long)e * a.out_pitch + tt] = o;
+    a.gpart[grp * cs + i] = o;
   }
   __syncthreads();
   for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
     const int e = i / a.zh, k = i - e * a.zh;
-    a.zhist[(long long)e * a.zh + k] = s_z[e * (a.zh + a.B) + a.B + k];
+    zh_g[i] = s_z[e * (a.zh + a.B) + a.B + k];
+  }
+  if (tid == 0) a.ticket[grp] = 0u;
+  // ---- level 2: the last group sums the groups' filtered blocks (fixed order)
+  if (!stream_last_arrival(a.ticket + groups, groups)) return;
+  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
+    const int e = i / a.B, tt = i - e * a.B;
+    float o = 0.f;
+    for (int g = 0; g < groups; ++g) o += __ldcg(a.gpart + g * cs + i);
+    a.out[(long long)e * a.out_pitch + tt] = o;
   }
   if (tid == 0) a.ticket[groups] = 0u;
+}
+
+__global__ void k_stream_gather_taps(const int2* __restrict__ raw, const int* __restrict__ nnz,
+                                     const int* __restrict__ src_dir, int S, int ears, int dirs, int stride,
+                                     int2* __restrict__ out, int* __restrict__ out_nnz) {
+  const long long total = (long long)S * ears * stride;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long se = i / stride;
+    const int k = (int)(i - se * stride);
+    const int s = (int)(se / ears), e = (int)(se - (long long)s * ears);
+    const long long row = (long long)e * dirs + src_dir[s];
+    out[i] = raw[row * stride + k];
+    if (k == 0) out_nnz[se] = nnz[row];
+  }
+}
+
+cudaError_t launch_stream_gather_taps(const int2* raw, const int* nnz, const int* src_dir, int S, int ears, int dirs,
+                                      int stride, int2* out, int* out_nnz, cudaStream_t st) {
+  const long long total = (long long)S * ears * stride;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 1024);
+  k_stream_gather_taps<<<std::max(blocks, 1), 256, 0, st>>>(raw, nnz, src_dir, S, ears, dirs, stride, out, out_nnz);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st) {

@@ -184,26 +184,26 @@ struct StreamArgs {
   int B;
   float* yhist;          // [S][H] last H samples of every source (H >= K-1, multiple of 4)
   int H;
-  const int* src_dir;
   int S;
-  const int2* taps;      // raw offsets (col = o)
-  const int* row_nnz;
+  const int2* src_taps;  // [S][ears][tap_stride] raw taps (col = o) of each source's direction
+  const int* src_nnz;    // [S][ears]
   int tap_stride;
-  int dirs;
   int ears;
   int src_per_cta;
-  float* part;           // [ctas][ears][B]
-  float* gpart;          // [ceil(ctas/16)][ears][B] level-1 sums
-  float* zhist;          // [ears][lf_pad] last lf_pad-? samples of z (H2 >= Lf-1)
-  int zh;                // history length of z (multiple of 16, >= Lf-1)
+  float* part;           // [ctas][ears][B] per-CTA z partials
+  float* gpart;          // [groups][ears][B] f * (group z)
+  float* zhist;          // [groups][ears][zh] last zh samples of each group's z
+  int zh;                // z history length (lf_pad >= Lf - 1)
   const float* f;        // [ears][lf_pad]
   int lf_pad;
   float* out;            // ear e at out + e * out_pitch, B samples
   long long out_pitch;
   int ctas;
-  unsigned int* ticket;  // [ceil(ctas/16) + 1] zero-initialised counters owned by the stream state
+  unsigned int* ticket;  // [groups + 1] zero-initialised counters owned by the stream state
   int* nonfinite;        // set to 1 when a non-finite input sample is read (may be null)
 };
+cudaError_t launch_stream_gather_taps(const int2* raw, const int* nnz, const int* src_dir, int S, int ears, int dirs,
+                                      int stride, int2* out, int* out_nnz, cudaStream_t st);
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st);
 
 }  // namespace toep

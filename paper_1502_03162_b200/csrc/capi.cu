@@ -649,6 +649,7 @@ struct toep_mixer {
   int* d_bsrc = nullptr;  // sources sorted by direction
   int* d_bptr = nullptr;  // bucket b = d_bsrc[d_bptr[b] .. d_bptr[b+1])
   int* d_bdir = nullptr;  // direction of bucket b
+  std::vector<int> h_bptr;
   float* d_part = nullptr;
   size_t part_bytes = 0;
 };
@@ -738,6 +739,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
       }
     }
     m->buckets = (int)bdir.size();
+    m->h_bptr = bptr;
     TOEP_CUDA(cudaMemcpyAsync(m->d_bsrc, ord.data(), count * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaMemcpyAsync(m->d_bptr, bptr.data(), bptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     TOEP_CUDA(cudaMemcpyAsync(m->d_bdir, bdir.data(), bdir.size() * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -753,7 +755,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     const long long slots = (long long)sm * (512 / (kR + g->kwin));
     // >= ~24 items per persistent CTA keeps the tail short; fewer groups keep the partials small
     long long bpg = ((long long)m->buckets * n_tiles + 24 * slots - 1) / (24 * slots);
-    bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, 512), m->buckets));  // <= kMixMaxBuckets
+    bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, kMixMaxBuckets), m->buckets));
     const int groups = (int)((m->buckets + bpg - 1) / bpg);
     TOEP_CUDA(ensure_part(m, (size_t)groups * m->r->ears * part_pitch * sizeof(float), st));
     MixArgs a{};
@@ -765,6 +767,10 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.bdir = m->d_bdir;
     a.buckets = m->buckets;
     a.buckets_per_group = (int)bpg;
+    int gsrc = 0;  // largest group's source count -> shared-memory table size (capped)
+    for (long long b0 = 0; b0 < m->buckets; b0 += bpg)
+      gsrc = std::max(gsrc, m->h_bptr[std::min<long long>(b0 + bpg, m->buckets)] - m->h_bptr[b0]);
+    a.group_srcs = (std::min(gsrc, kMixGroupSrcCap) + 3) & ~3;
     a.groups = groups;
     a.n_tiles = n_tiles;
     a.n_items = (long long)groups * n_tiles;

@@ -135,7 +135,6 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st) {
 //      accumulating the item's z quarter in registers.
 // No CTA barrier inside the bucket loop (only when the group's tables
 // change), so warps drift freely; partials leave once per item.
-constexpr int kMixMaxBuckets = 512;   // buckets per group (shared-memory tables)
 
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
@@ -145,30 +144,33 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 
-constexpr int kMixGroupSrcs = 1024;
+constexpr int kMixSlots = 4;  // sources per bucket prefetched into shared-memory slots
 
 struct MixLayout {
-  int warp_floats, slice_off, slot_off, taps_off, bptr_off, bdir_off, bsrc_off, total_bytes;
+  int warp_floats, slot_floats, slot_off, taps_off, bptr_off, bdir_off, boff_off, total_bytes;
 };
 
-__host__ __device__ inline MixLayout mix_layout(int KWIN, int tap_stride) {
+// Per warp: kMixSlots source slots (slot 0 doubles as the bank-padded sum
+// slice once the bucket's sources are summed) and two tap-row buffers; per
+// CTA: the group's bucket tables, sources as 64-bit row offsets.
+__host__ __device__ inline MixLayout mix_layout(int KWIN, int tap_stride, int bpg, int group_srcs) {
   MixLayout L{};
   const int slice = 32 * kR + KWIN;
   const int v4 = (slice / 4 + 31) / 32;
-  L.slice_off = 0;  // padded [slice]
-  int off = (padded_len(slice) + 31) & ~31;
-  L.slot_off = off;  // [SLOTS][32 lanes * v4] float4 (lane-private)
-  off += 3 * 4 * 32 * v4;
+  const int lanes = 4 * 32 * v4;  // lane-column layout of a slot
+  L.slot_floats = ((padded_len(slice) > lanes ? padded_len(slice) : lanes) + 31) & ~31;
+  L.slot_off = 0;  // [SLOTS][slot_floats]
+  int off = kMixSlots * L.slot_floats;
   L.taps_off = off;  // [2 buffers][tap_stride] int4 ear pairs
   off += 2 * 4 * tap_stride;
   L.warp_floats = (off + 31) & ~31;
   off = kWarps * L.warp_floats;
+  L.boff_off = off;  // [group_srcs] int64
+  off += 2 * group_srcs;
   L.bptr_off = off;
-  off += kMixMaxBuckets + 4;
+  off += (bpg + 4) & ~3;
   L.bdir_off = off;
-  off += kMixMaxBuckets;
-  L.bsrc_off = off;
-  off += kMixGroupSrcs;
+  off += (bpg + 3) & ~3;
   L.total_bytes = off * 4;
   return L;
 }
@@ -178,18 +180,19 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
   constexpr int COLS = kR + KWIN;
   constexpr int SLICE = 32 * kR + KWIN;
   constexpr int V4 = (SLICE / 4 + 31) / 32;
-  constexpr int SLOTS = 3;
+  constexpr int SLOTS = kMixSlots;
   extern __shared__ __align__(128) float smem[];
   __shared__ unsigned s_tbase;
-  const MixLayout L = mix_layout(KWIN, a.tap_stride);
+  const MixLayout L = mix_layout(KWIN, a.tap_stride, a.buckets_per_group, a.group_srcs);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* wb = smem + warp * L.warp_floats;
-  float* s_slice = wb + L.slice_off;
-  float4* s_slot = reinterpret_cast<float4*>(wb + L.slot_off);
+  float* s_slots = wb + L.slot_off;
+  float* s_slice = s_slots;  // slot 0 after the sum
   int4* s_taps = reinterpret_cast<int4*>(wb + L.taps_off);  // [2 buffers][tap_stride] ear pairs
+  long long* s_boff = reinterpret_cast<long long*>(smem + L.boff_off);
   int* s_bptr = reinterpret_cast<int*>(smem + L.bptr_off);
   int* s_bdir = reinterpret_cast<int*>(smem + L.bdir_off);
-  int* s_bsrc = reinterpret_cast<int*>(smem + L.bsrc_off);
+  const int SF = L.slot_floats;
   if (warp == 0) tmem_alloc<COLS>(&s_tbase);
   tmem_fence_before();
   __syncthreads();
@@ -211,13 +214,15 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       for (int i = tid; i < nb; i += kThreads) s_bdir[i] = __ldg(a.bdir + b0 + i);
       gfirst = __ldg(a.bptr + b0);
       const int gn = __ldg(a.bptr + b0 + nb) - gfirst;
-      src_in_smem = gn <= kMixGroupSrcs;
+      src_in_smem = gn <= a.group_srcs;
       if (src_in_smem)
-        for (int i = tid; i < gn; i += kThreads) s_bsrc[i] = __ldg(a.bsrc + gfirst + i);
+        for (int i = tid; i < gn; i += kThreads) s_boff[i] = (long long)__ldg(a.bsrc + gfirst + i) * a.y_pitch;
       __syncthreads();
       tab_grp = grp;
     }
-    auto src_at = [&](int i) { return src_in_smem ? s_bsrc[i - gfirst] : __ldg(a.bsrc + i); };
+    auto src_off = [&](int i) {  // row offset of the i-th source of the bucket order
+      return src_in_smem ? s_boff[i - gfirst] : (long long)__ldg(a.bsrc + i) * a.y_pitch;
+    };
     const long long T0 = (long long)j * kW;
     const long long w0 = T0 + (long long)warp * 32 * kR - KWIN;  // signal index of s_slice[0]
     const bool interior = w0 >= 0 && w0 + SLICE <= a.T;
@@ -225,11 +230,12 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       const int i0 = s_bptr[k], n = min(s_bptr[k + 1] - i0, SLOTS);
       if (interior) {
         for (int u = 0; u < n; ++u) {
-          const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i0 + u) * a.y_pitch + w0);
+          const float4* ys = reinterpret_cast<const float4*>(a.y + src_off(i0 + u) + w0);
+          float4* sl = reinterpret_cast<float4*>(s_slots + u * SF);
 #pragma unroll
           for (int q = 0; q < V4; ++q) {
             const int c = lane + 32 * q;
-            if (c < SLICE / 4) cp_async16(&s_slot[u * 32 * V4 + c], ys + c);
+            if (c < SLICE / 4) cp_async16(&sl[c], ys + c);
           }
         }
       }
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
             for (int q = 0; q < V4; ++q) {
               const int c = lane + 32 * q;
               if (c < SLICE / 4) {
-                const float4 l = s_slot[u * 32 * V4 + c];
+                const float4 l = reinterpret_cast<const float4*>(s_slots + u * SF)[c];
                 fadd2(v[q].x, v[q].y, l.x, l.y);
                 fadd2(v[q].z, v[q].w, l.z, l.w);
               }
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
           }
         }
         for (int i = i0 + SLOTS; i < i1; ++i) {
-          const float4* ys = reinterpret_cast<const float4*>(a.y + (long long)src_at(i) * a.y_pitch + w0);
+          const float4* ys = reinterpret_cast<const float4*>(a.y + src_off(i) + w0);
 #pragma unroll
           for (int q = 0; q < V4; ++q) {
             const int c = lane + 32 * q;
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
         }
       } else {
         for (int i = i0; i < i1; ++i) {
-          const float* ys = a.y + (long long)src_at(i) * a.y_pitch;
+          const float* ys = a.y + src_off(i);
 #pragma unroll
           for (int q = 0; q < V4; ++q) {
             const int c = lane + 32 * q;
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
         ffma2(chk0, chk1, v[q].x, v[q].y, 0.f);
         ffma2(chk0, chk1, v[q].z, v[q].w, 0.f);
       }
-      __syncwarp();  // previous bucket's window reads of s_slice are done; tap rows of k visible
+      __syncwarp();  // every lane's slot reads are done: slot 0 takes the sum; tap rows of k visible
       {
         float* sb = s_slice + padi(4 * lane);  // padi(4*(lane + 32q)) = padi(4*lane) + 144q
 #pragma unroll
@@ -311,7 +317,6 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       __syncwarp();
       const int4* tp = s_taps + (k & 1) * a.tap_stride;
       const int dir = s_bdir[k];
-      if (k + 1 < nb) prefetch(k + 1);  // next bucket's loads overlap this bucket's taps
       {
 #pragma unroll
         for (int c = 0; c < COLS; c += 16) {
@@ -328,6 +333,8 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
         }
         tmem_wait_st();
       }
+      __syncwarp();                     // the slice (slot 0) has been read
+      if (k + 1 < nb) prefetch(k + 1);  // next bucket's loads overlap this bucket's taps
       const float keepB = a.ears > 1 ? 1.f : 0.f;
       if constexpr (NNZT > 0) {
         float XA0[16], XB0[16], XA1[16], XB1[16];
@@ -403,11 +410,15 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
 
 template <int KWIN, int NNZT>
 static cudaError_t launch_mix_t(const MixArgs& a, int sm_count, cudaStream_t st) {
-  const int bytes = mix_layout(KWIN, a.tap_stride).total_bytes;
+  const int bytes = mix_layout(KWIN, a.tap_stride, a.buckets_per_group, a.group_srcs).total_bytes;
   auto kern = k_mix<KWIN, NNZT>;
   cudaError_t err = ensure_smem(reinterpret_cast<const void*>(kern), bytes);
   if (err != cudaSuccess) return err;
-  long long grid = (long long)sm_count * (512 / (kR + KWIN));  // TMEM-bounded co-residency
+  static int smem_sm = 0;  // co-resident CTAs: TMEM allows 512 / COLS, shared memory may allow fewer
+  if (!smem_sm && cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0) != cudaSuccess)
+    smem_sm = 228 * 1024;
+  const int per_sm = std::max(1, std::min(512 / (kR + KWIN), smem_sm / (bytes + 2048)));  // + static + reserved
+  long long grid = (long long)sm_count * per_sm;
   if (grid > a.n_items) grid = a.n_items;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, kThreads, bytes, st>>>(a);

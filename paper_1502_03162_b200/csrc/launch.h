@@ -146,6 +146,8 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st);
 //   part[grp][e][t] = sum_{s in grp} sum_k v_{e,d(s),k} * y_s[t - o_{e,d(s),k}]
 // Bucketed mix (one pass over the sources): buckets are the sets of sources
 // sharing a direction; item = (bucket group, 2048-sample tile).
+constexpr int kMixMaxBuckets = 512;    // buckets per group
+constexpr int kMixGroupSrcCap = 1024;  // largest shared-memory source table
 struct MixArgs {
   const float* y;        // sources, row s at y + s * y_pitch, length T
   long long T;
@@ -155,6 +157,7 @@ struct MixArgs {
   const int* bdir;       // [buckets] direction of each bucket
   int buckets;
   int buckets_per_group;
+  int group_srcs;        // shared-memory source-table capacity (a larger group reads bsrc from HBM)
   int groups;
   int n_tiles;           // ceil(zlen / 2048)
   long long n_items;     // groups * n_tiles

@@ -731,9 +731,9 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     for (int i = 0; i < count; ++i) ord[i] = i;
     const int* dir = m->h_dir.data() + s0;
     std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
-    std::vector<int> bptr(1, 0), bdir;
+    std::vector<int> bptr(1, 0), bdir;  // a direction with more than kMixGroupSrcCap sources spans several buckets
     for (int p = 0; p < count; ++p) {
-      if (p + 1 == count || dir[ord[p + 1]] != dir[ord[p]]) {
+      if (p + 1 == count || dir[ord[p + 1]] != dir[ord[p]] || p + 1 - bptr.back() == kMixGroupSrcCap) {
         bdir.push_back(dir[ord[p]]);
         bptr.push_back(p + 1);
       }
@@ -756,6 +756,14 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     // >= ~24 items per persistent CTA keeps the tail short; fewer groups keep the partials small
     long long bpg = ((long long)m->buckets * n_tiles + 24 * slots - 1) / (24 * slots);
     bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, kMixMaxBuckets), m->buckets));
+    auto group_srcs = [&](long long per) {  // largest source count of a group of `per` buckets
+      int g = 0;
+      for (long long b0 = 0; b0 < m->buckets; b0 += per)
+        g = std::max(g, m->h_bptr[std::min<long long>(b0 + per, m->buckets)] - m->h_bptr[b0]);
+      return g;
+    };
+    int gsrc = group_srcs(bpg);
+    while (gsrc > kMixGroupSrcCap && bpg > 1) gsrc = group_srcs(bpg = (bpg + 1) / 2);  // the tables live in smem
     const int groups = (int)((m->buckets + bpg - 1) / bpg);
     TOEP_CUDA(ensure_part(m, (size_t)groups * m->r->ears * part_pitch * sizeof(float), st));
     MixArgs a{};
@@ -767,10 +775,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.bdir = m->d_bdir;
     a.buckets = m->buckets;
     a.buckets_per_group = (int)bpg;
-    int gsrc = 0;  // largest group's source count -> shared-memory table size (capped)
-    for (long long b0 = 0; b0 < m->buckets; b0 += bpg)
-      gsrc = std::max(gsrc, m->h_bptr[std::min<long long>(b0 + bpg, m->buckets)] - m->h_bptr[b0]);
-    a.group_srcs = (std::min(gsrc, kMixGroupSrcCap) + 3) & ~3;
+    a.group_srcs = (gsrc + 3) & ~3;
     a.groups = groups;
     a.n_tiles = n_tiles;
     a.n_items = (long long)groups * n_tiles;

@@ -63,6 +63,17 @@ __device__ __forceinline__ void tmem_st16(unsigned ta, const float (&d)[16]) {
       : "memory");
 }
 
+// Same store without a compiler memory barrier: it reads registers only, so
+// shared-memory loads that feed later stores may be hoisted above it (its
+// order against other tcgen05 ops is that of the volatile asm statements).
+__device__ __forceinline__ void tmem_st16_nb(unsigned ta, const float (&d)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7]), "f"(d[8]),
+      "f"(d[9]), "f"(d[10]), "f"(d[11]), "f"(d[12]), "f"(d[13]), "f"(d[14]), "f"(d[15]));
+}
+
 // One lane of the (converged) warp; lets ptxas issue uniform-datapath ops
 // (UTMA*/UBLKCP) without a per-lane serialisation loop.
 __device__ __forceinline__ bool elect_one() {

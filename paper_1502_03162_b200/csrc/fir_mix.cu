@@ -204,7 +204,6 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
   const long long it1 = min(a.n_items, it0 + per);
   int grp = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)grp * a.n_tiles);
   int tab_grp = -1, gfirst = 0;
-  bool src_in_smem = false;
   float chk0 = 0.f, chk1 = 0.f;
   for (long long item = it0; item < it1; ++item) {
     const int b0 = grp * a.buckets_per_group, nb = min(a.buckets - b0, a.buckets_per_group);
@@ -214,15 +213,12 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       for (int i = tid; i < nb; i += kThreads) s_bdir[i] = __ldg(a.bdir + b0 + i);
       gfirst = __ldg(a.bptr + b0);
       const int gn = __ldg(a.bptr + b0 + nb) - gfirst;
-      src_in_smem = gn <= a.group_srcs;
-      if (src_in_smem)
-        for (int i = tid; i < gn; i += kThreads) s_boff[i] = (long long)__ldg(a.bsrc + gfirst + i) * a.y_pitch;
+      for (int i = tid; i < gn; i += kThreads) s_boff[i] = (long long)__ldg(a.bsrc + gfirst + i) * a.y_pitch;
       __syncthreads();
       tab_grp = grp;
     }
-    auto src_off = [&](int i) {  // row offset of the i-th source of the bucket order
-      return src_in_smem ? s_boff[i - gfirst] : (long long)__ldg(a.bsrc + i) * a.y_pitch;
-    };
+    const long long* boff = s_boff - gfirst;  // row offset of the i-th source in bucket order: boff[i]
+    auto src_off = [&](int i) { return boff[i]; };
     const long long T0 = (long long)j * kW;
     const long long w0 = T0 + (long long)warp * 32 * kR - KWIN;  // signal index of s_slice[0]
     const bool interior = w0 >= 0 && w0 + SLICE <= a.T;
@@ -320,16 +316,18 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
       {
 #pragma unroll
         for (int c = 0; c < COLS; c += 16) {
+          // 16 | (16 * lane + c), so padi(16 * lane + c + 4q) = padi(16 * lane + c) + 4q
+          const float4* row = reinterpret_cast<const float4*>(&s_slice[padi(16 * lane + c)]);
           float w[16];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 t4 = *reinterpret_cast<const float4*>(&s_slice[padi(16 * lane + c + 4 * q)]);
+            const float4 t4 = row[q];
             w[4 * q] = t4.x;
             w[4 * q + 1] = t4.y;
             w[4 * q + 2] = t4.z;
             w[4 * q + 3] = t4.w;
           }
-          tmem_st16(tlane + c, w);
+          tmem_st16_nb(tlane + c, w);
         }
         tmem_wait_st();
       }

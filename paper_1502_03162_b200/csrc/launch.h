@@ -147,7 +147,7 @@ cudaError_t launch_sparse_generic(const SparseGenericArgs& a, cudaStream_t st);
 // Bucketed mix (one pass over the sources): buckets are the sets of sources
 // sharing a direction; item = (bucket group, 2048-sample tile).
 constexpr int kMixMaxBuckets = 512;    // buckets per group
-constexpr int kMixGroupSrcCap = 1024;  // largest shared-memory source table
+constexpr int kMixGroupSrcCap = 1024;  // sources per bucket group (host splits larger buckets)
 struct MixArgs {
   const float* y;        // sources, row s at y + s * y_pitch, length T
   long long T;
@@ -157,7 +157,7 @@ struct MixArgs {
   const int* bdir;       // [buckets] direction of each bucket
   int buckets;
   int buckets_per_group;
-  int group_srcs;        // shared-memory source-table capacity (a larger group reads bsrc from HBM)
+  int group_srcs;        // shared-memory source-table capacity (>= every group's source count)
   int groups;
   int n_tiles;           // ceil(zlen / 2048)
   long long n_items;     // groups * n_tiles

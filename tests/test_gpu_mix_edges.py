@@ -40,11 +40,19 @@ def test_large_buckets(mods):
 
 
 def test_one_direction_many_sources(mods):
-    """One bucket of 2,100 sources: the group's source list exceeds the shared-memory table."""
+    """One direction with 2,100 sources: split into buckets of <= 1,024 (the shared-memory source table)."""
     from paper_1502_03162_b200.synth import Config
     cfg = Config("o", ny=3_000, M=200, K=100, nnz=16, dirs=4, ears=2, sources=2100)
     sd = np.full(cfg.sources, 2, np.int32)
     _mix_check(mods, cfg, sd, 202, [(0, 3199)])
+
+
+def test_bucket_groups_shrink_to_fit_table(mods):
+    """~75 sources per direction: 16-bucket groups would hold ~1,200 sources, so the host halves the group."""
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("g", ny=2_500, M=200, K=100, nnz=24, dirs=40, ears=2, sources=3000)
+    sd = np.random.default_rng(4).integers(0, cfg.dirs, size=cfg.sources).astype(np.int32)
+    _mix_check(mods, cfg, sd, 303, [(0, 900), (2_000, 699)])
 
 
 def test_mono_and_uneven_nnz(mods):

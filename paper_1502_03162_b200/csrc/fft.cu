@@ -180,13 +180,16 @@ __global__ void k_pack_real(const float* __restrict__ x, long long nx, float2* _
 
 // ---------------------------------------------------------------- host ----
 // Twiddle tables exp(-2 pi i k / n), k < n/2, computed in double on the host,
-// cached per (n, precision) for the process lifetime.
+// cached per (device, n, precision) for the process lifetime.
 static std::mutex g_tw_mu;
 static std::unordered_map<long long, void*> g_tw;
 
 static cudaError_t twiddles(long long n, bool dbl, const void** out) {
+  int dev = 0;
+  cudaError_t ed = cudaGetDevice(&dev);
+  if (ed != cudaSuccess) return ed;
   std::lock_guard<std::mutex> lk(g_tw_mu);
-  const long long key = n * 2 + (dbl ? 1 : 0);
+  const long long key = ((long long)dev << 48) | (n * 2 + (dbl ? 1 : 0));
   auto it = g_tw.find(key);
   if (it != g_tw.end()) {
     *out = it->second;

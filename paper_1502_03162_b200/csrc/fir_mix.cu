@@ -412,8 +412,10 @@ static cudaError_t launch_mix_t(const MixArgs& a, int sm_count, cudaStream_t st)
   auto kern = k_mix<KWIN, NNZT>;
   cudaError_t err = ensure_smem(reinterpret_cast<const void*>(kern), bytes);
   if (err != cudaSuccess) return err;
-  static int smem_sm = 0;  // co-resident CTAs: TMEM allows 512 / COLS, shared memory may allow fewer
-  if (!smem_sm && cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0) != cudaSuccess)
+  // co-resident CTAs: TMEM allows 512 / COLS, shared memory may allow fewer
+  int dev = 0, smem_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess)
     smem_sm = 228 * 1024;
   const int per_sm = std::max(1, std::min(512 / (kR + KWIN), smem_sm / (bytes + 2048)));  // + static + reserved
   long long grid = (long long)sm_count * per_sm;

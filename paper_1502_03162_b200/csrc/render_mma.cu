@@ -579,7 +579,10 @@ cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, in
   cfg.numAttrs = 1;
   // persistent: exactly the clusters that can be co-resident (GPC sizes need
   // not be multiples of the cluster size), one CTA per SM
-  static int max_clusters = 0;
+  static int clusters_per_dev[64] = {0};  // per device (GPC layouts may differ)
+  int dev = 0;
+  if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
+  int& max_clusters = clusters_per_dev[dev & 63];
   if (max_clusters == 0) {
     cfg.gridDim = dim3((unsigned)(std::max(1, sm_count / kMmaCluster) * kMmaCluster));
     if (cudaOccupancyMaxActiveClusters(&max_clusters, k_render_mma, &cfg) != cudaSuccess || max_clusters < 1)

@@ -77,7 +77,8 @@ int toep_taps_create(int32_t rows, int32_t length, const int64_t* row_ptr, const
                      const float* values, toep_taps** out);
 int toep_taps_destroy(toep_taps* t);
 int toep_taps_info(const toep_taps* t, int32_t* rows, int32_t* length, int32_t* max_nnz, int64_t* total_nnz);
-/* One row of a table against one device signal: out[0 .. ny+length-1). */
+/* One row of a table against one device signal: out[0 .. ny+length-1),
+ * exactly (nothing past the end is written; any alignment). */
 int toep_taps_conv(const toep_taps* t, int32_t row, const float* y, int64_t ny, float* out, void* stream);
 
 /* ---- renderer: resonance f per ear + reflection table rows ear-major ----- */
@@ -113,9 +114,13 @@ int toep_renderer_path(const toep_renderer* r);
  * nonfinite == NULL only clears it (stream-ordered, no wait).
  * (Reflection lengths > 497 take the banded fallback, which is not covered.) */
 int toep_renderer_check(const toep_renderer* r, int32_t* nonfinite, void* stream);
-/* Stage 2 only, rows [row0, row0+nrows) of one ear against a precomputed
- * y*f (length nyf): the per-direction reflection convolution of
- * Renderer.render once the resonance cache is warm (engine/__init__.py:252-260). */
+/* Stage 2 only, every direction of one ear against a precomputed y*f
+ * (length nyf): the per-direction reflection convolution of Renderer.render
+ * once the resonance cache is warm (engine/__init__.py:252-260).  Row d at
+ * out + d*out_pitch, nyf+K-1 samples; with more than one direction the tail
+ * of a row up to the next multiple of 4 samples may be written (zeros), so
+ * out_pitch % 4 == 0 and out 16-byte aligned; a single direction is written
+ * exactly (any alignment). */
 int toep_renderer_reflect(const toep_renderer* r, int32_t ear, const float* yf, int64_t nyf, float* out,
                           int64_t out_pitch, void* stream);
 

@@ -209,8 +209,22 @@ int toep_taps_info(const toep_taps* t, int32_t* rows, int32_t* length, int32_t* 
 // all reading the same input signal x (nx samples).  `pairs`/`pnnz` are the
 // rows' pair-interleaved taps (k_pair_taps); null -> built here for this call.
 static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pairs, const int4* pnnz, const float* x,
-                        long long nx, float* out, long long out_pitch, cudaStream_t st, int* nonfinite = nullptr) {
+                        long long nx, float* out, long long out_pitch, cudaStream_t st, int* nonfinite = nullptr,
+                        bool padded_out = false) {
   const long long out_len = nx + t->length - 1;
+  if (t->kwin > 0 && nrows == 1 && !padded_out && (out_len % 4 != 0 || !aligned16(out))) {
+    // one row, exactly out_len samples: the kernel's stores move whole 16-byte
+    // units, so it renders into a padded scratch row that is copied out exact
+    float* row = nullptr;
+    TOEP_CUDA(cudaMallocAsync(&row, (size_t)round_up(out_len, 4) * sizeof(float), st));
+    int rc = reflect_rows(t, row0, 1, pairs, pnnz, x, nx, row, 0, st, nonfinite, true);
+    if (rc == TOEP_OK) {
+      cudaError_t e = cudaMemcpyAsync(out, row, (size_t)out_len * sizeof(float), cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) rc = cuda_fail(e, "copy of the rendered row");
+    }
+    cudaFreeAsync(row, st);
+    return rc;
+  }
   if (t->kwin > 0) {
     if (!aligned16(out) || (nrows > 1 && out_pitch % 4 != 0))
       return fail(TOEP_ERR_INVALID, "output must be 16-byte aligned with a pitch multiple of 4");

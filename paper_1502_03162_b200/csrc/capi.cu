@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -51,6 +52,38 @@ int sm_count_cached() {
 
 inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Stream-ordered allocations come from a per-device pool that keeps freed
+// memory (release threshold = max): the default pool hands memory back to the
+// driver at every synchronisation, so a per-call scratch buffer after a host
+// sync paid a fresh mapping (~10 ms measured on the numpy Renderer.render path).
+cudaMemPool_t scratch_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  return pools[dev];
+}
+
+template <class T>
+cudaError_t pool_alloc(T** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool = scratch_pool();
+  if (!pool) return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, st);
+}
 
 }  // namespace
 
@@ -135,10 +168,10 @@ static int taps_build(int32_t rows, int32_t length, const int64_t* row_ptr, cons
   }
   cudaError_t e;
   if (stream_owned) {
-    e = cudaMallocAsync(&t->d_kw, n * sizeof(int2), st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&t->d_raw, n * sizeof(int2), st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&t->d_nnz, rows * sizeof(int), st);
-    if (e == cudaSuccess && !rp.empty()) e = cudaMallocAsync(&t->d_rowpairs, rp.size() * sizeof(int4), st);
+    e = pool_alloc(&t->d_kw, n * sizeof(int2), st);
+    if (e == cudaSuccess) e = pool_alloc(&t->d_raw, n * sizeof(int2), st);
+    if (e == cudaSuccess) e = pool_alloc(&t->d_nnz, rows * sizeof(int), st);
+    if (e == cudaSuccess && !rp.empty()) e = pool_alloc(&t->d_rowpairs, rp.size() * sizeof(int4), st);
   } else {
     e = cudaMalloc(&t->d_kw, n * sizeof(int2));
     if (e == cudaSuccess) e = cudaMalloc(&t->d_raw, n * sizeof(int2));
@@ -216,7 +249,7 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pai
     // one row, exactly out_len samples: the kernel's stores move whole 16-byte
     // units, so it renders into a padded scratch row that is copied out exact
     float* row = nullptr;
-    TOEP_CUDA(cudaMallocAsync(&row, (size_t)round_up(out_len, 4) * sizeof(float), st));
+    TOEP_CUDA(pool_alloc(&row, (size_t)round_up(out_len, 4) * sizeof(float), st));
     int rc = reflect_rows(t, row0, 1, pairs, pnnz, x, nx, row, 0, st, nonfinite, true);
     if (rc == TOEP_OK) {
       cudaError_t e = cudaMemcpyAsync(out, row, (size_t)out_len * sizeof(float), cudaMemcpyDeviceToDevice, st);
@@ -231,7 +264,7 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pai
     const int P = (nrows + 1) / 2;
     int4* tmp = nullptr;
     if (!pairs) {
-      TOEP_CUDA(cudaMallocAsync(&tmp, (size_t)P * (t->tap_stride + 1) * sizeof(int4), st));
+      TOEP_CUDA(pool_alloc(&tmp, (size_t)P * (t->tap_stride + 1) * sizeof(int4), st));
       cudaError_t ep = launch_pair_taps(t->d_kw + (size_t)row0 * t->tap_stride, t->d_nnz + row0, 1, nrows,
                                         t->tap_stride, t->kwin, tmp, tmp + (size_t)P * t->tap_stride, st);
       if (ep != cudaSuccess) {
@@ -325,7 +358,7 @@ int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps
   const long long nh_pad = round_up(ntaps, 16);
   if (nh_pad > (1LL << 30)) return fail(TOEP_ERR_UNSUPPORTED, "too many taps");
   float* h = nullptr;
-  TOEP_CUDA(cudaMallocAsync(&h, nh_pad * sizeof(float), st));
+  TOEP_CUDA(pool_alloc(&h, nh_pad * sizeof(float), st));
   cudaError_t e = cudaMemsetAsync(h, 0, nh_pad * sizeof(float), st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, taps, ntaps * sizeof(float), cudaMemcpyDeviceToDevice, st);
   int rc = (e == cudaSuccess) ? dense_fir(y, ny, 0, h, (int)nh_pad, 0, 1, out, ny + ntaps - 1, 0, st)
@@ -368,7 +401,7 @@ int toep_fft(const double* in, double* out, int64_t n, int inverse, int64_t* mac
   double* dst = out;
   double* tmp = nullptr;
   if (in == out && fft_needs_distinct(n, true)) {
-    TOEP_CUDA(cudaMallocAsync(&tmp, (size_t)n * 2 * sizeof(double), st));
+    TOEP_CUDA(pool_alloc(&tmp, (size_t)n * 2 * sizeof(double), st));
     dst = tmp;
   }
   cudaError_t e = launch_fft_c128(in, dst, n, inverse != 0, st);
@@ -382,7 +415,7 @@ int toep_fft_spectrum(const float* taps, int64_t ntaps, int64_t n, float* spectr
   if (ntaps < 1 || ntaps > n || !taps || !spectrum) return fail(TOEP_ERR_INVALID, "bad taps for a %lld-point spectrum", (long long)n);
   cudaStream_t st = S(stream);
   float* tmp = nullptr;
-  TOEP_CUDA(cudaMallocAsync(&tmp, (size_t)n * 2 * sizeof(float), st));
+  TOEP_CUDA(pool_alloc(&tmp, (size_t)n * 2 * sizeof(float), st));
   cudaError_t e = launch_fft_spectrum(taps, ntaps, n, spectrum, tmp, st);
   cudaFreeAsync(tmp, st);
   return e == cudaSuccess ? TOEP_OK : cuda_fail(e, "toep_fft_spectrum");
@@ -397,7 +430,7 @@ int toep_fft_conv(const float* y, int64_t ny, const float* spectrum, int64_t n, 
   cudaStream_t st = S(stream);
   const long long sb = fft_conv_scratch_bytes(ny, n, ntaps);
   float* scratch = nullptr;
-  if (sb > 0) TOEP_CUDA(cudaMallocAsync(&scratch, (size_t)sb, st));
+  if (sb > 0) TOEP_CUDA(pool_alloc(&scratch, (size_t)sb, st));
   cudaError_t e = launch_fft_conv(y, ny, spectrum, n, ntaps, out, scratch, st);
   if (scratch) cudaFreeAsync(scratch, st);
   return e == cudaSuccess ? TOEP_OK : cuda_fail(e, "toep_fft_conv");
@@ -614,7 +647,7 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
   const long long nyf = ny + r->lf - 1;
   const long long pitch = round_up(nyf, 4);
   float* yf = nullptr;
-  TOEP_CUDA(cudaMallocAsync(&yf, (size_t)pitch * r->ears * sizeof(float), st));
+  TOEP_CUDA(pool_alloc(&yf, (size_t)pitch * r->ears * sizeof(float), st));
   int rc = TOEP_OK;
   for (int e = 0; e < r->ears && rc == TOEP_OK; ++e)
     rc = dense_fir(y, ny, 0, r->d_f + (size_t)e * r->lf_pad, r->lf_pad, 0, 1, yf + e * pitch, nyf, 0, st);

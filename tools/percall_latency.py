@@ -29,3 +29,23 @@ for label, fn, ndir in [("engine.render (new Renderer each call)", lambda d: eng
         out = fn(100 + i if ndir == 1250 else i % ndir)
     torch.cuda.synchronize()
     print("%-45s %.3f ms/call" % (label, (time.perf_counter() - t0) / n * 1e3))
+
+# ConvPlan / convolve in each mode (plan built once; numpy in/out)
+taps = np.random.default_rng(3).standard_normal(200)
+for mode, bs in [("dense_direct", None), ("fft_overlap_save", 1024), ("fft_overlap_save", 4096)]:
+    plan = engine.ConvPlan(taps, mode, block_size=bs)
+    for i in range(5):
+        engine.convolve(plan, y)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(50):
+        engine.convolve(plan, y)
+    print("%-45s %.3f ms/call" % ("convolve %s%s" % (mode, "" if bs is None else " block %d" % bs),
+                                  (time.perf_counter() - t0) / 50 * 1e3))
+sp = engine.ConvPlan(ms[0].reflections[0], "sparse_direct")
+for i in range(5):
+    engine.convolve(sp, y)
+t0 = time.perf_counter()
+for i in range(50):
+    engine.convolve(sp, y)
+print("%-45s %.3f ms/call" % ("convolve sparse_direct (K=100, nnz 16)", (time.perf_counter() - t0) / 50 * 1e3))

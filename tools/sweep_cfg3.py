@@ -1,6 +1,6 @@
 """BASELINE config 3: sparsity / length sweep on one B200.
 
-    python tools/sweep_cfg3.py [--steps 10] [--check]
+    python tools/sweep_cfg3.py [--steps 10] [--check] [--only 150:16,100:16]
 
 y = 441,000 samples, 1,250 directions x 2 ears, K in {50, 100, 150}
 (Lf = 201 - K), nnz in {4, 8, 16, 32, 64} plus the dense control nnz = K
@@ -25,7 +25,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--check", action="store_true", help="oracle parity on 4 rows per point")
+    ap.add_argument("--only", default="", help="comma list of K:nnz points, e.g. 150:16,150:150")
     args = ap.parse_args()
+    only = {tuple(int(v) for v in p.split(":")) for p in args.only.split(",") if p}
     import torch
 
     from bench import _peaks, timed, _flush_fn
@@ -36,6 +38,8 @@ def main():
     fp32 = sm * 128 * 2 * peaks["sm_max_mhz"] * 1e6
     flush = _flush_fn()
     for cfg in synth.cfg3_points():
+        if only and (cfg.K, cfg.nnz) not in only:
+            continue
         ms = synth.models(cfg, seed=cfg.K * 1000 + cfg.nnz)
         y = torch.from_numpy(synth.source(cfg.ny, seed=3).astype(np.float32)).cuda()
         br = batch.BatchRenderer(ms)

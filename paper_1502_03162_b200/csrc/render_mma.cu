@@ -189,7 +189,7 @@ __host__ __device__ inline MmaSmem mma_smem_n(int kpad, int lf_pad, int nstg) {
   L.sc_off = off;
   off += 8 * 4;
   L.bars_off = off;
-  off += (12 + 2 * kMmaBStages) * 8;
+  off += (12 + 2 * kMmaBStages + 5) * 8;
   L.total = off + 1024;  // alignment slack
   L.nstg = nstg;
   return L;
@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   const int KP = a.kpad, KS = KP / 16, NA = mma_a_buffers(KP);
+  const bool ring = NA == 1 && kMmaAccCols + 3 * (KP / 2) <= 512;
   const MmaSmem L = mma_smem(KP, a.lf_pad);
   const int b_part_bytes = kMmaN * KP * 2;
   const int b_chunk_bytes = 2 * b_part_bytes;
@@ -228,6 +229,13 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
   uint64_t* sc_empty = bars + 10;  // [2]
   uint64_t* b_full = bars + 12;    // [kMmaBStages]
   uint64_t* b_empty = b_full + kMmaBStages;
+  // ring mode (one A buffer does not leave room for two): hi and lo halves of
+  // successive items rotate through three KP/2-column slots; item i's hi goes
+  // to slot (2i) % 3 and its lo to (2i+1) % 3, so the next item's hi is written
+  // while this item runs and its lo as soon as this item's hi MMAs retire.
+  // a_full doubles as hi_full.
+  uint64_t* lo_full = b_empty + kMmaBStages;  // [2]
+  uint64_t* slot_free = lo_full + 2;          // [3]
   __shared__ unsigned s_tbase;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -245,6 +253,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       mbar_init(&sc_full[i], 1);
       mbar_init(&sc_empty[i], kMmaEpiWarps);
     }
+    for (int i = 0; i < 2; ++i) mbar_init(&lo_full[i], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&slot_free[i], 1);
     for (int i = 0; i < kMmaBStages; ++i) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], kMmaCluster);  // every CTA of the cluster frees the stage
@@ -296,28 +306,41 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     // ===== MMA issuer =====
     if (elect_one()) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(kMmaN >> 3) << 17) | ((uint32_t)(kMmaM >> 4) << 24);
-      int bs = 0, as = 0, ab = -1;
+      int bs = 0, as = 0, ab = -1, nit = -1;
       unsigned bph = 0, aph = 0, a_ph[2] = {0u, 0u};
       long long cur = -1;
       const unsigned sb = smem_u32(sB);
       for (long long u = u0; u < u1; ++u) {
         const long long item = u / nch;
+        const int cu = (int)(u - item * nch);
         if (item != cur) {
-          if (ab >= 0) mma_commit(&a_empty[ab]);  // this A buffer is free once its MMAs retire
-          ab = (ab + 1) % NA;
-          PW(1, mbar_wait_sleep(&a_full[ab], a_ph[ab]));
-          a_ph[ab] ^= 1u;
+          ++nit;
+          if (ring) {
+            PW(1, mbar_wait_sleep(&a_full[nit & 1], (unsigned)((nit >> 1) & 1)));  // hi rows of item nit
+          } else {
+            if (ab >= 0) mma_commit(&a_empty[ab]);  // this A buffer is free once its MMAs retire
+            ab = (ab + 1) % NA;
+            PW(1, mbar_wait_sleep(&a_full[ab], a_ph[ab]));
+            a_ph[ab] ^= 1u;
+          }
           cur = item;
         }
         PW(2, mbar_wait_sleep(&b_full[bs], bph));
         PW(3, mbar_wait_sleep(&acc_empty[as], aph ^ 1u));
         tmem_fence_after();
         const unsigned d = tbase + (unsigned)(as * kMmaN);
-        const unsigned at = tbase + (unsigned)(kMmaAccCols + ab * KP);  // [hi | lo] KP/2 columns each
+        const int hs = (2 * nit) % 3, ls = (2 * nit + 1) % 3;
+        const unsigned at = tbase + (unsigned)(kMmaAccCols + (ring ? 0 : ab * KP));  // [hi | lo] KP/2 columns each
+        const unsigned a_hi = ring ? at + (unsigned)(hs * (KP / 2)) : at;
+        const unsigned a_lo = ring ? at + (unsigned)(ls * (KP / 2)) : at + (unsigned)(KP / 2);
         int acc = 0;
 #pragma unroll 1
         for (int p = 0; p < 3; ++p) {  // hi*hi, hi*lo, lo*hi
-          const unsigned pa = at + (unsigned)(p == 2 ? KP / 2 : 0);
+          if (ring && p == 2) {
+            if (cu == nch - 1) mma_commit(&slot_free[hs]);  // the item's hi rows are done
+            if (cu == 0) PW(1, mbar_wait_sleep(&lo_full[nit & 1], (unsigned)((nit >> 1) & 1)));
+          }
+          const unsigned pa = p == 2 ? a_lo : a_hi;
           const unsigned pb = sb + (unsigned)(bs * b_chunk_bytes + (p == 1 ? 1 : 0) * b_part_bytes);
           for (int ks = 0; ks < KS; ++ks) {
 #if !TOEP_MMA_NOMMA
@@ -326,6 +349,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             acc = 1;
           }
         }
+        if (ring && cu == nch - 1) mma_commit(&slot_free[ls]);  // and its lo rows
         mma_commit_multicast(&b_empty[bs], cmask);
         mma_commit(&acc_full[as]);
         if (++bs == kMmaBStages) {
@@ -389,6 +413,39 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         PW(5, mbar_wait_sleep(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1)));
         s_sc[nitem & 1] = ldexpf(1.f, -sexp);
         mbar_arrive(&sc_full[nitem & 1]);
+      }
+      if (ring) {
+        // hi rows into slot (2i) % 3, then lo rows into (2i+1) % 3, each once
+        // the MMAs of its previous occupant have retired (use k of a slot
+        // waits for completion k-1 of slot_free; a fresh barrier passes k = 0)
+        const float* src = s_yf + (32 * q + lane + KP - 1);
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {
+          const int g = 2 * nitem + part, slot = g % 3, k = g / 3;
+          PW(4, mbar_wait_sleep(&slot_free[slot], (unsigned)((k & 1) ^ 1)));
+          tmem_fence_after();
+          const unsigned ta = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(kMmaAccCols + slot * (KP / 2));
+#pragma unroll 1
+          for (int gi = g0; gi < g1; ++gi) {
+            const int j0 = 8 * gi;
+            unsigned w[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float x0 = src[-2 * (j0 + j)] * scale, x1 = src[-2 * (j0 + j) - 1] * scale;
+              const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+              w[j] = part == 0 ? pack_half2(h0, h1)
+                               : pack_half2(__float2half_rn(x0 - __half2float(h0)),
+                                            __float2half_rn(x1 - __half2float(h1)));
+            }
+            tmem_st8(ta + j0, w);
+          }
+          tmem_wait_st();
+          tmem_fence_before();
+          builders_sync();
+          if (bt == 0) mbar_arrive(part == 0 ? &a_full[nitem & 1] : &lo_full[nitem & 1]);
+        }
+        ++nitem;
+        continue;
       }
       // the MMAs that last read this A buffer must have retired
       PW(4, mbar_wait_sleep(&a_empty[ab], a_ph[ab] ^ 1u));

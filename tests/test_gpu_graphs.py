@@ -1,0 +1,79 @@
+"""GPU: the batched entry points are stream-ordered and capturable.
+
+A serving loop records the render / mix once in a CUDA graph and replays it
+per request; the C ABI must therefore do no host synchronisation or
+allocation on those paths once the device state exists (the fused non-finite
+check reads a flag back, so it is switched off inside the capture).  Replays
+must reproduce the eager results bit for bit, on a new input written into
+the captured buffer.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mods(cuda):
+    from paper_1502_03162_b200 import batch, synth
+    return batch, synth, cuda
+
+
+def _capture(torch, fn):
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()  # warm: first-use setup (tensor maps, smem attributes) outside the capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    return g
+
+
+@pytest.mark.parametrize("K,nnz,path", [(100, 16, "tensor"), (150, 16, "tensor"), (150, 4, "window")])
+def test_render_all_in_a_graph(mods, K, nnz, path):
+    batch, synth, torch = mods
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("g", ny=20_000, M=K + 100 if K > 100 else 200, K=K, nnz=nnz, dirs=133, ears=2)
+    ms = synth.models(cfg, seed=K + nnz)
+    br = batch.BatchRenderer(ms)
+    assert br.native.path() == path
+    y = torch.from_numpy(synth.source(cfg.ny, seed=1).astype(np.float32)).cuda()
+    out = br.alloc(cfg.ny)
+    g = _capture(torch, lambda: br.render_all(y, out=out, check_finite=False))
+    y.copy_(torch.from_numpy(synth.source(cfg.ny, seed=2).astype(np.float32)).cuda())
+    out.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    got = out.clone()
+    want = br.render_all(y, out=br.alloc(cfg.ny))
+    L = br.out_len(cfg.ny)
+    assert torch.equal(got[:, :, :L], want[:, :, :L])
+
+
+def test_mix_in_a_graph(mods):
+    batch, synth, torch = mods
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("m", ny=30_000, M=200, K=100, nnz=24, dirs=60, ears=2, sources=90)
+    ms = synth.models(cfg, seed=4)
+    sd = np.random.default_rng(4).integers(0, cfg.dirs, size=cfg.sources).astype(np.int32)
+    mix = batch.MixRenderer(ms, sd, cfg.ny)
+    y = synth.device_sources(cfg.sources, cfg.ny, seed=5)
+    z = mix.alloc_z()
+    out = torch.empty((cfg.ears, (mix.out_len + 3) // 4 * 4), device="cuda")
+
+    def step():
+        z.zero_()
+        mix.partial(y, z=z, check_finite=False)
+        mix.finish(z, out=out)
+
+    g = _capture(torch, step)
+    synth.device_sources(cfg.sources, cfg.ny, seed=6, out=y)
+    out.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    got = out[:, :mix.out_len].clone()
+    want = mix.render(y)
+    assert torch.equal(got, want)

@@ -346,7 +346,8 @@ def run_reference(args, world, rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE laws)",
         "config": {"workload": wl, "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind, "sample": desc,
+                         "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -522,6 +523,17 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     return line
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_line(workload):
     cores = os.cpu_count() or 1
     step, desc, kind, pool, single = reference_step_factory(workload if workload in ("cfg1", "cfg2", "cfg4", "cfg5")
@@ -542,7 +554,7 @@ def cpu_baseline_line(workload):
         pool.join()
     return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": kind,
             "sample": "%s; %d repetitions" % (desc, reps), "seconds": dt,
-            "single_core_value": single(3.0)}
+            "single_core_value": single(3.0), "cpu_model": _cpu_model()}
 
 
 def main():

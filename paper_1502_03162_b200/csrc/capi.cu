@@ -697,6 +697,7 @@ struct toep_mixer {
   int* d_bptr = nullptr;  // bucket b = d_bsrc[d_bptr[b] .. d_bptr[b+1])
   int* d_bdir = nullptr;  // direction of bucket b
   std::vector<int> h_bptr;
+  unsigned long long* d_work = nullptr;  // k_mix item counter
   float* d_part = nullptr;
   size_t part_bytes = 0;
 };
@@ -739,6 +740,7 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
   cudaError_t e = cudaMalloc(&m->d_bsrc, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bptr, (n_src + 1) * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bdir, n_src * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_work, sizeof(unsigned long long));
   if (e != cudaSuccess) {
     toep_mixer_destroy(m);
     return cuda_fail(e, "toep_mixer_create");
@@ -752,6 +754,7 @@ int toep_mixer_destroy(toep_mixer* m) {
   if (m->d_bsrc) cudaFree(m->d_bsrc);
   if (m->d_bptr) cudaFree(m->d_bptr);
   if (m->d_bdir) cudaFree(m->d_bdir);
+  if (m->d_work) cudaFree(m->d_work);
   if (m->d_part) cudaFree(m->d_part);
   delete m;
   return TOEP_OK;
@@ -836,6 +839,8 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.part_pitch = part_pitch;
     a.zlen = m->zlen;
     a.nonfinite = m->r->d_nonfinite;
+    a.work = m->d_work;
+    TOEP_CUDA(cudaMemsetAsync(m->d_work, 0, sizeof(unsigned long long), st));
     cudaError_t e = launch_mix(a, g->kwin, g->uniform ? g->max_nnz : 0, sm, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_mix");
     e = launch_mix_reduce(m->d_part, groups, m->r->ears, part_pitch, m->zlen, z, z_pitch, st);

@@ -144,7 +144,8 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 
-constexpr int kMixSlots = 4;  // sources per bucket prefetched into shared-memory slots
+constexpr int kMixSlots = 4;
+  // sources per bucket prefetched into shared-memory slots
 
 struct MixLayout {
   int warp_floats, slot_floats, slot_off, taps_off, bptr_off, bdir_off, boff_off, total_bytes;
@@ -199,13 +200,18 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
   tmem_fence_after();
   const unsigned tlane = s_tbase + ((unsigned)(32 * warp) << 16);
 
-  const long long per = (a.n_items + gridDim.x - 1) / gridDim.x;
-  const long long it0 = (long long)blockIdx.x * per;
-  const long long it1 = min(a.n_items, it0 + per);
-  int grp = (int)(it0 / a.n_tiles), j = (int)(it0 - (long long)grp * a.n_tiles);
+  // Items in tile-major order (consecutive items walk the groups of one
+  // tile), handed out dynamically: thread 0 takes the next item from a global
+  // counter, so CTAs finish together whatever their groups' source counts.
+  __shared__ long long s_item;
   int tab_grp = -1, gfirst = 0;
   float chk0 = 0.f, chk1 = 0.f;
-  for (long long item = it0; item < it1; ++item) {
+  for (;;) {
+    if (tid == 0) s_item = (long long)atomicAdd(a.work, 1ull);
+    __syncthreads();
+    const long long item = s_item;
+    if (item >= a.n_items) break;
+    const int j = (int)(item / a.groups), grp = (int)(item - (long long)j * a.groups);
     const int b0 = grp * a.buckets_per_group, nb = min(a.buckets - b0, a.buckets_per_group);
     if (grp != tab_grp) {  // the group's bucket tables -> shared memory (all warps at this item)
       __syncthreads();
@@ -393,10 +399,7 @@ __global__ void __launch_bounds__(kThreads, 512 / (kR + KWIN)) k_mix(MixArgs a) 
         for (int r = 0; r < 16; r += 4) pB[r / 4] = make_float4(accB[r], accB[r + 1], accB[r + 2], accB[r + 3]);
       }
     }
-    if (++j == a.n_tiles) {
-      j = 0;
-      ++grp;
-    }
+    __syncthreads();  // s_item is rewritten for the next item
   }
   cp_async_wait_all();
   const bool bad = !isfinite(chk0 + chk1);

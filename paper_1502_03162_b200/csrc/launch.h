@@ -168,6 +168,7 @@ struct MixArgs {
   int dirs;
   int ears;
   float* part;           // [groups][ears][part_pitch]
+  unsigned long long* work;  // item counter for dynamic scheduling (zeroed before the launch), or null
   long long part_pitch;
   long long zlen;        // T + K - 1
   int* nonfinite;        // set to 1 when a non-finite source sample is read (may be null)

@@ -804,7 +804,8 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     const int sm = sm_count_cached();
     const long long slots = (long long)sm * (512 / (kR + g->kwin));
     // >= ~24 items per persistent CTA keeps the tail short; fewer groups keep the partials small
-    long long bpg = ((long long)m->buckets * n_tiles + 24 * slots - 1) / (24 * slots);
+    const long long ipc = 24;  // items per CTA (12 / 48 / 96 measured no better)
+    long long bpg = ((long long)m->buckets * n_tiles + ipc * slots - 1) / (ipc * slots);
     bpg = std::max(16LL, std::min<long long>(std::min<long long>(bpg, kMixMaxBuckets), m->buckets));
     auto group_srcs = [&](long long per) {  // largest source count of a group of `per` buckets
       int g = 0;

@@ -70,6 +70,7 @@ struct RenderMmaArgs {
   int nchunks;           // ceil(dirs / render_mma_chunk())
   int dirs, ears;
   int n_titems;          // ceil(out_len / 128)
+  int t_begin, t_end;    // this launch's 128-output tiles of every ear (set by launch_render_mma)
   float* out;            // row (e * dirs + d) at out + row * out_pitch
   long long out_pitch;
   long long out_len;

@@ -45,6 +45,7 @@
 //                 [32 directions][32 t] blocks in shared memory, TMA tensor
 //                 stores (3-D map {t, direction, ear} clips padding directions)
 #include <algorithm>
+#include <mutex>
 #include <cstdio>
 #include <cuda_fp16.h>
 
@@ -205,6 +206,7 @@ __host__ __device__ inline MmaSmem mma_smem(int kpad, int lf_pad) {
 // item's Hankel rows are written while this item's MMAs run), else one
 __host__ __device__ inline int mma_a_buffers(int kpad) { return kMmaAccCols + 2 * kpad <= 512 ? 2 : 1; }
 
+template <int CL>
 __global__ void __launch_bounds__(kMmaThreads, 1)
     k_render_mma(RenderMmaArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ unsigned char smraw[];
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     for (int i = 0; i < 3; ++i) mbar_init(&slot_free[i], 1);
     for (int i = 0; i < kMmaBStages; ++i) {
       mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], kMmaCluster);  // every CTA of the cluster frees the stage
+      mbar_init(&b_empty[i], CL);  // every CTA of the cluster frees the stage
     }
     mbar_fence_init();
   }
@@ -273,12 +275,12 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
   // store nothing.
   const int nch = a.nchunks;
   const int crank = (int)cluster_ctarank();
-  const long long gpe = (a.n_titems + kMmaCluster - 1) / kMmaCluster;  // groups per ear
+  const long long gpe = (a.t_end - a.t_begin + CL - 1) / CL;  // groups per ear (this launch's tiles)
   const long long ngroups = gpe * a.ears;
   const long long g0 = ngroups * cluster_id_x() / num_clusters_x();
   const long long g1 = ngroups * (cluster_id_x() + 1) / num_clusters_x();
   const long long u0 = g0 * nch, u1 = g1 * nch;
-  const unsigned short cmask = (unsigned short)((1u << kMmaCluster) - 1u);
+  const unsigned short cmask = (unsigned short)((1u << CL) - 1u);
 
   if (warp == 0) {
     // ===== G chunk producer =====
@@ -292,8 +294,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         PW(0, mbar_wait_sleep(&b_empty[bs], bph ^ 1u));  // the stage is free in every CTA of the cluster
         mbar_arrive_expect_tx(&b_full[bs], (unsigned)b_chunk_bytes);
         // this CTA loads one 16-byte-aligned slice of the chunk for the whole cluster
-        const int sl0 = (int)((long long)b_chunk_bytes / 16 * crank / kMmaCluster) * 16;
-        const int sl1 = (int)((long long)b_chunk_bytes / 16 * (crank + 1) / kMmaCluster) * 16;
+        const int sl0 = (int)((long long)b_chunk_bytes / 16 * crank / CL) * 16;
+        const int sl1 = (int)((long long)b_chunk_bytes / 16 * (crank + 1) / CL) * 16;
         bulk_load_multicast(sB + bs * b_chunk_bytes + sl0, g + ((long long)e * nch + c) * b_chunk_bytes + sl0,
                             (unsigned)(sl1 - sl0), &b_full[bs], cmask);
         if (++bs == kMmaBStages) {
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       if (item == cur) continue;
       cur = item;
       const int ab = nitem % NA;
-      const int e = (int)(item / gpe), ti = (int)(item % gpe) * kMmaCluster + crank;
+      const int e = (int)(item / gpe), ti = a.t_begin + (int)(item % gpe) * CL + crank;
       const long long T0 = (long long)ti * kMmaM;
       const long long y0 = T0 - (KP - 1) - (a.lf_pad - 1);
       if (e != cur_e)
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     for (long long u = u0; u < u1; ++u) {
       const long long item = u / nch;
       const int c = (int)(u % nch);
-      const int e = (int)(item / gpe), ti = (int)(item % gpe) * kMmaCluster + crank;
+      const int e = (int)(item / gpe), ti = a.t_begin + (int)(item % gpe) * CL + crank;
       if (item != cur) {
         if (nitem >= 0) {
           __syncwarp();
@@ -509,7 +511,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       tmem_fence_after();
       const long long t0 = (long long)ti * kMmaM + 32 * q;
       const float unscale_c = unscale * __ldg(a.gscale + (long long)e * nch + c);  // tile 2^-s x chunk 2^-q
-      if (t0 < a.out_len) {
+      if (t0 < a.out_len && ti < a.t_end) {
 #pragma unroll 1
         for (int blk = 0; blk < 2; ++blk) {
           const int col = 64 * half + 32 * blk;  // accumulator column = direction within the chunk
@@ -619,37 +621,103 @@ cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st) {
-  const MmaSmem L = mma_smem(a.kpad, a.lf_pad);
-  cudaError_t err = ensure_smem(reinterpret_cast<const void*>(k_render_mma), L.total);
-  if (err != cudaSuccess) return err;
-  cudaLaunchConfig_t cfg = {};
+template <int CL>
+static void mma_cluster_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int smem) {
+  cfg = {};
   cfg.blockDim = dim3(kMmaThreads);
-  cfg.dynamicSmemBytes = (size_t)L.total;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cfg.dynamicSmemBytes = (size_t)smem;
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kMmaCluster;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // persistent: exactly the clusters that can be co-resident (GPC sizes need
-  // not be multiples of the cluster size), one CTA per SM
-  static int clusters_per_dev[64] = {0};  // per device (GPC layouts may differ)
-  int dev = 0;
-  if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
-  int& max_clusters = clusters_per_dev[dev & 63];
-  if (max_clusters == 0) {
-    cfg.gridDim = dim3((unsigned)(std::max(1, sm_count / kMmaCluster) * kMmaCluster));
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, k_render_mma, &cfg) != cudaSuccess || max_clusters < 1)
-      max_clusters = std::max(1, sm_count / kMmaCluster);
-    cudaGetLastError();
-  }
-  cfg.gridDim = dim3((unsigned)(max_clusters * kMmaCluster));
-  err = cudaLaunchKernelEx(&cfg, k_render_mma, a, map);
+}
+
+template <int CL>
+static cudaError_t launch_mma_cl(const RenderMmaArgs& a, const CUtensorMap& map, int grid, int smem, cudaStream_t st) {
+  cudaError_t err = ensure_smem(reinterpret_cast<const void*>(k_render_mma<CL>), smem);
+  if (err != cudaSuccess) return err;
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr[1];
+  mma_cluster_cfg<CL>(cfg, attr, smem);
+  cfg.stream = st;
+  cfg.gridDim = dim3((unsigned)grid);
+  err = cudaLaunchKernelEx(&cfg, k_render_mma<CL>, a, map);
   if (err != cudaSuccess) return err;
   return cudaGetLastError();
+}
+
+template <int CL>
+static int max_clusters_for(int sm_count, int smem) {
+  if (ensure_smem(reinterpret_cast<const void*>(k_render_mma<CL>), smem) != cudaSuccess) return 1;
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr[1];
+  mma_cluster_cfg<CL>(cfg, attr, smem);
+  cfg.gridDim = dim3((unsigned)(std::max(1, sm_count / CL) * CL));
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_render_mma<CL>, &cfg) != cudaSuccess || n < 1) n = std::max(1, sm_count / CL);
+  cudaGetLastError();
+  return n;
+}
+
+#ifndef TOEP_MMA_FILL
+#define TOEP_MMA_FILL 1
+#endif
+#ifndef TOEP_MMA_FILL_RATE
+#define TOEP_MMA_FILL_RATE 1.0
+#endif
+#ifndef TOEP_MMA_FILL_CL
+#define TOEP_MMA_FILL_CL 2
+#endif
+constexpr int kMmaFillCluster = TOEP_MMA_FILL_CL;
+
+// Persistent launch: exactly the kMmaCluster-CTA clusters that can be
+// co-resident (GPC sizes are not multiples of 6: 22 clusters cover 132 of a
+// B200's 148 SMs), plus, concurrently on a side stream, small clusters on the
+// SMs left over; each launch takes a share of every ear's tiles in proportion
+// to its measured throughput.
+cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st) {
+  const MmaSmem L = mma_smem(a.kpad, a.lf_pad);
+  struct Fill {  // per device: the cluster count and the side stream/events of the fill launch
+    int clusters = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+  };
+  static std::mutex mu;
+  static Fill fills[64];
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);  // fork -> launches -> join is one unit per call
+  Fill& F = fills[dev];
+  if (!F.clusters) {
+    if ((err = cudaStreamCreateWithFlags(&F.side, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    if ((err = cudaEventCreateWithFlags(&F.fork, cudaEventDisableTiming)) != cudaSuccess) return err;
+    if ((err = cudaEventCreateWithFlags(&F.join, cudaEventDisableTiming)) != cudaSuccess) return err;
+    F.clusters = max_clusters_for<kMmaCluster>(sm_count, L.total);
+    if (getenv("TOEP_VERBOSE"))
+      fprintf(stderr, "k_render_mma: %d clusters of %d CTAs + fill on %d SMs\n", F.clusters, kMmaCluster, sm_count);
+  }
+  const int main_ctas = F.clusters * kMmaCluster;
+  const int fill = TOEP_MMA_FILL ? (sm_count - main_ctas) / kMmaFillCluster * kMmaFillCluster : 0;
+  RenderMmaArgs m = a;
+  m.t_begin = 0;
+  m.t_end = a.n_titems;
+  if (fill <= 0 || a.n_titems < 4 * sm_count) return launch_mma_cl<kMmaCluster>(m, map, main_ctas, L.total, st);
+  const double share = main_ctas / (main_ctas + TOEP_MMA_FILL_RATE * fill);
+  const int split = std::min(a.n_titems, ((int)(a.n_titems * share) + kMmaCluster - 1) / kMmaCluster * kMmaCluster);
+  m.t_end = split;
+  RenderMmaArgs f = a;
+  f.t_begin = split;
+  f.t_end = a.n_titems;
+  if ((err = cudaEventRecord(F.fork, st)) != cudaSuccess) return err;
+  if ((err = cudaStreamWaitEvent(F.side, F.fork, 0)) != cudaSuccess) return err;
+  if ((err = launch_mma_cl<kMmaCluster>(m, map, main_ctas, L.total, st)) != cudaSuccess) return err;
+  if ((err = launch_mma_cl<kMmaFillCluster>(f, map, fill, L.total, F.side)) != cudaSuccess) return err;
+  if ((err = cudaEventRecord(F.join, F.side)) != cudaSuccess) return err;
+  return cudaStreamWaitEvent(st, F.join, 0);
 }
 
 }  // namespace toep

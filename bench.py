@@ -407,7 +407,8 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
     roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": _traffic(workload),
             "peak_src": peaks["src"],
-            "kernel": {"tensor": "k_render_mma (tcgen05.mma split-fp16, TMA-multicast G)",
+            "kernel": {"tensor": "k_render_mma (tcgen05.mma split-fp16, TMA-multicast G; 6-CTA clusters + a concurrent "
+                                 "2-CTA-cluster launch on the SMs they leave idle)",
                        "window": "k_render<112,true,16> (TMEM window + FFMA2)",
                        "banded": "k_sparse_generic"}[br.native.path()],
             "fp32_tflops": flops / (kern_ms * 1e-3) / 1e12,
@@ -442,7 +443,7 @@ def bench_cfg2(args, world, rank, local, workload="cfg2"):
                    "samples_per_step": samples_global,
                    "parallelism": "independent sources x %d (one per GPU)" % world,
                    "l2": "flushed between steps (256 MiB write)"},
-        "roofline": roof, "e2e": e2e, "gpu_launches": args.steps,
+        "roofline": roof, "e2e": e2e, "gpu_launches": args.steps * br.native.kernels(cfg.ny),
         "clocks": clk.summary(),
     }
     return line

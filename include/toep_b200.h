@@ -106,6 +106,10 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
 #define TOEP_PATH_WINDOW 0
 #define TOEP_PATH_BANDED 2
 int toep_renderer_path(const toep_renderer* r);
+/* Kernel launches one toep_renderer_render call makes for a signal of ny
+ * samples (the tensor path adds a concurrent launch on the SMs its clusters
+ * leave idle; the banded path runs one FIR per ear first). */
+int toep_renderer_kernels(const toep_renderer* r, int64_t ny);
 /* Fused input check (the reference's DataError "signal contains non-finite
  * samples", engine/__init__.py:162-165): every render / reflect / mixer /
  * streamer kernel made from this renderer ORs a device flag when it reads an

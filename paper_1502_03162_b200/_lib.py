@@ -25,6 +25,7 @@ EXPORTS = (
     "toep_taps_create", "toep_taps_destroy", "toep_taps_info", "toep_taps_conv",
     "toep_renderer_create", "toep_renderer_destroy", "toep_renderer_out_len", "toep_renderer_min_pitch",
     "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check", "toep_renderer_path",
+    "toep_renderer_kernels",
     "toep_mixer_create", "toep_mixer_destroy", "toep_mixer_z_len", "toep_mixer_out_len",
     "toep_mixer_partial", "toep_mixer_finish",
     "toep_streamer_create", "toep_streamer_destroy", "toep_streamer_reset", "toep_streamer_step",
@@ -80,6 +81,7 @@ def load_library(path: str = LIB_PATH):
         "toep_renderer_reflect": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp, _i64, _vp]),
         "toep_renderer_check": (ctypes.c_int, [_vp, _i32p, _vp]),
         "toep_renderer_path": (ctypes.c_int, [_vp]),
+        "toep_renderer_kernels": (ctypes.c_int, [_vp, ctypes.c_int64]),
         "toep_mixer_create": (ctypes.c_int, [_vp, _i32p, _i32, _i64, ctypes.POINTER(_vp)]),
         "toep_mixer_destroy": (ctypes.c_int, [_vp]),
         "toep_mixer_z_len": (_i64, [_vp]),
@@ -227,6 +229,10 @@ class NativeRenderer:
                                                   stream_ptr(stream)))
 
     PATHS = {1: "tensor", 0: "window", 2: "banded"}
+
+    def kernels(self, ny: int) -> int:
+        """Kernel launches render() makes for a signal of ny samples."""
+        return int(load_library().toep_renderer_kernels(self._h, int(ny)))
 
     def path(self) -> str:
         """Which stage-2 kernel render() launches: "tensor" (tcgen05 GEMM), "window" (TMEM + FFMA2), "banded"."""

@@ -549,6 +549,19 @@ static int renderer_path(const toep_renderer* r) {
 
 int toep_renderer_path(const toep_renderer* r) { return r ? renderer_path(r) : -1; }
 
+int toep_renderer_kernels(const toep_renderer* r, int64_t ny) {
+  if (!r || ny < 1) return -1;
+  switch (renderer_path(r)) {
+    case TOEP_PATH_TENSOR:
+      return render_mma_launches((int)((toep_renderer_out_len(r, ny) + 127) / 128), render_mma_kpad(r->g->length),
+                                 r->lf_pad, sm_count_cached());
+    case TOEP_PATH_WINDOW:
+      return 1;
+    default:
+      return r->ears + 1;  // k_fir per ear, then k_sparse_generic
+  }
+}
+
 int toep_renderer_check(const toep_renderer* r, int32_t* nonfinite, void* stream) {
   if (!r) return fail(TOEP_ERR_INVALID, "null renderer");
   cudaStream_t st = S(stream);

@@ -85,6 +85,7 @@ cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, i
 cudaError_t make_render_mma_map(float* out, int ears, int dirs, long long out_len, long long out_pitch,
                                 CUtensorMap* m);
 cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st);
+int render_mma_launches(int n_titems, int kpad, int lf_pad, int sm_count);
 
 // FFT (fft.cu): radix-2, power-of-two n; complex buffers interleaved.
 cudaError_t launch_fft_c128(const double* in, double* out, long long n, bool inverse, cudaStream_t st);

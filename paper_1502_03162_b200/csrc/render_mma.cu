@@ -672,6 +672,15 @@ static int max_clusters_for(int sm_count, int smem) {
 #endif
 constexpr int kMmaFillCluster = TOEP_MMA_FILL_CL;
 
+// Kernel launches one launch_render_mma call makes for this many tiles (1, or
+// 2 with the fill launch on the SMs the clusters leave idle).
+int render_mma_launches(int n_titems, int kpad, int lf_pad, int sm_count) {
+  const MmaSmem L = mma_smem(kpad, lf_pad);
+  const int main_ctas = max_clusters_for<kMmaCluster>(sm_count, L.total) * kMmaCluster;
+  const int fill = TOEP_MMA_FILL ? (sm_count - main_ctas) / kMmaFillCluster * kMmaFillCluster : 0;
+  return (fill > 0 && n_titems >= 4 * sm_count) ? 2 : 1;
+}
+
 // Persistent launch: exactly the kMmaCluster-CTA clusters that can be
 // co-resident (GPC sizes are not multiples of 6: 22 clusters cover 132 of a
 // B200's 148 SMs), plus, concurrently on a side stream, small clusters on the

@@ -108,3 +108,15 @@ def test_shape_envelope(mods, K, lf, dirs, ears):
         ref = oracle.render_rows(y, f, model_rows(models), K, dirs)
         for r in range(ears * dirs):
             assert rel_l2(out[r], ref[r]) <= TOL, (ny, r, br.native.path())
+
+
+def test_kernel_count_query(mods):
+    """toep_renderer_kernels: what bench.py reports as gpu_launches."""
+    batch, synth, model_rows = mods
+    from paper_1502_03162_b200.synth import Config
+    br = batch.BatchRenderer(synth.models(Config("k", ny=1000, M=200, K=100, nnz=16, dirs=8, ears=2), seed=1))
+    assert br.native.path() == "tensor"
+    assert br.native.kernels(1000) == 1           # small renders: the clustered launch alone
+    assert br.native.kernels(441_000) in (1, 2)   # + the fill launch when clusters leave SMs idle
+    bw = batch.BatchRenderer(synth.models(Config("w", ny=1000, M=250, K=150, nnz=4, dirs=8, ears=2), seed=1))
+    assert bw.native.path() == "window" and bw.native.kernels(441_000) == 1

@@ -44,7 +44,11 @@ def report(path):
     rows = list(csv.reader(io.StringIO(src)))
     if len(rows) > 2:
         h = rows[1]
-        data = rows[2:]
+        data = []
+        for r in rows[2:]:  # the first kernel's section (a report may hold several)
+            if r and r[0] == "Kernel Name":
+                break
+            data.append(r)
         si, wi, ei = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
         tot = sum(float(r[wi] or 0) for r in data) or 1.0
         ex = sum(float(r[ei] or 0) for r in data) or 1.0
@@ -56,6 +60,7 @@ def report(path):
             op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
             cs[op] += float(r[wi] or 0)
             ce[op] += float(r[ei] or 0)
+        print("  (SASS source page, first kernel of the report)")
         print("  executed-instruction mix:", ", ".join("%s %.1f%%" % (k, 100 * v / ex) for k, v in ce.most_common(10)))
         print("  stall-sample share by opcode:", ", ".join("%s %.1f%%" % (k, 100 * v / tot) for k, v in cs.most_common(10)))
 

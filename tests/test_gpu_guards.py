@@ -184,3 +184,31 @@ def test_conv_sparse_exact_length(mods, K, nnz):
     dense = np.zeros(K)
     dense[idx] = val
     assert rel_l2(out.cpu().numpy(), np.convolve(y.astype(np.float64), dense)) <= TOL
+
+
+def test_render_long_signal_two_launches_stay_in_bounds(mods):
+    """Long signals add the fill launch (its own tile range of every row): both stay inside the rows."""
+    batch, synth, model_rows, torch = mods
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("L", ny=300_003, M=200, K=100, nnz=16, dirs=9, ears=2)
+    ms = synth.models(cfg, seed=77)
+    br = batch.BatchRenderer(ms)
+    assert br.native.path() == "tensor"
+    y = synth.source(cfg.ny, seed=78)
+    L = br.out_len(cfg.ny)
+    mp = br.native.min_pitch(cfg.ny)
+    pitch = mp + 8
+    buf, out = _guarded(torch, (cfg.ears, cfg.dirs, pitch))
+    br.render_all(torch.from_numpy(y.astype(np.float32)).cuda(), out=out)
+    torch.cuda.synchronize()
+    assert _bands_intact(buf, out.numel())
+    host = out.cpu().numpy()
+    tail = host[:, :, L:mp]
+    assert (np.isnan(tail) | (tail == 0)).all() and np.isnan(host[:, :, mp:]).all()
+    assert not np.isnan(host[:, :, :L]).any()
+    f = np.stack([m.resonance_taps for m in ms])
+    rows = np.array([0, 8, 9, 17], np.int32)
+    ref = oracle.render_rows(y, f, model_rows(ms), cfg.K, cfg.dirs, rows=rows)
+    flat = host.reshape(-1, pitch)
+    for i, r in enumerate(rows):
+        assert rel_l2(flat[r, :L], ref[i]) <= TOL, r

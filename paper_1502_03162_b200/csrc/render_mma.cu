@@ -26,10 +26,14 @@
 // pair {A[t][2j], A[t][2j+1]}), so each MMA reads only G from shared memory
 // (with A in shared memory the MMAs were shared-memory-bandwidth bound); two
 // A buffers when KPAD <= 128, so the next tile's rows are written while this
-// tile's MMAs run.  G chunks are shared by a cluster of kMmaCluster CTAs that
-// render consecutive tiles in lockstep: each CTA loads 1/kMmaCluster of every
-// chunk with a multicast bulk copy, and each CTA's MMA completion frees the
-// stage in all of them (tcgen05.commit .multicast::cluster).
+// tile's MMAs run (at KPAD 160 the hi / lo halves rotate through three TMEM
+// slots instead).  G chunks are shared by a cluster of CL CTAs that render
+// consecutive tiles in lockstep: each CTA loads 1/CL of every chunk with a
+// multicast bulk copy, and each CTA's MMA completion frees the stage in all
+// of them (tcgen05.commit .multicast::cluster).  A render is one launch of
+// 6-CTA clusters (22 fit a B200's GPCs: 132 SMs) plus a concurrent launch of
+// 2-CTA clusters on the 16 SMs left, each over its own share of every ear's
+// tiles (launch_render_mma).
 //
 // Persistent, warp-specialised CTA (one per SM, 18 warps):
 //   warp 0      : TMA producer -- its slice of each G chunk (canonical fp16

@@ -509,6 +509,33 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
             "alg_bytes_per_launch": bytes_local, "distinct_directions": int(ndist),
             "fp32_tflops": flops_local / (kern_ms * 1e-3) / 1e12,
             "fp32_frac": flops_local / (kern_ms * 1e-3) / 1e12 / fp32_peak}
+    # e2e: the rank's sources from pinned host memory every step (H2D inside
+    # the timed region), the mix through the public API, the stereo result
+    # back to the host on rank 0
+    e2e = None
+    if not args.no_e2e:
+        try:
+            y_pin = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+            y_pin.copy_(y)
+            out_pin = torch.empty(outb.shape, dtype=torch.float32, pin_memory=True)
+
+            def e2e_step():
+                y.copy_(y_pin, non_blocking=True)
+                r = mix.partial(y, z=z)  # the user's call: includes the fused non-finite check
+                tdist.reduce_partials(z, dst=0, group=group)
+                if rank == 0:
+                    mix.finish(z, out=outb)
+                    out_pin.copy_(outb, non_blocking=True)
+                return r
+
+            ms_e2e, _ = timed(e2e_step, 2, 1, world)
+            e2e_ms = _max_over_ranks(sum(ms_e2e), world)
+            e2e = {"value": samples * 2 / (e2e_ms * 1e-3), "unit": "samples/s",
+                   "h2d_bytes_per_step": int(y_pin.numel() * 4) * world,
+                   "d2h_bytes_per_step": int(out_pin.numel() * 4), "ms_per_step": e2e_ms / 2}
+            del y_pin, out_pin
+        except RuntimeError as err:  # pinning 47 GB / world of host memory can fail on small hosts
+            e2e = {"value": None, "unavailable": "pinned host buffer: %s" % str(err).splitlines()[0]}
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True,
@@ -518,7 +545,7 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
                    "nnz": cfg.nnz, "ears": cfg.ears,
                    "parallelism": "sources by direction/%d + nccl reduce" % world,
                    "l2": "inputs (47 GB) larger than L2; flushed between steps"},
-        "roofline": roof, "e2e": None, "gpu_launches": args.steps * (3 if rank == 0 else 2),
+        "roofline": roof, "e2e": e2e, "gpu_launches": args.steps * (3 if rank == 0 else 2),
         "clocks": clk.summary(),
     }
     return line

@@ -321,6 +321,18 @@ def _probe_ref():
     return oracle.ref_kernels() is not None
 
 
+def _workload_config(wl, sample):
+    """The config keys our arm reports for this workload, plus the reference sample note."""
+    from paper_1502_03162_b200 import synth
+    cfg = synth.CONFIGS.get(wl, synth.CONFIGS["cfg2"])
+    d = {"workload": wl, "sources": cfg.sources, "directions": cfg.dirs, "ears": cfg.ears, "signal_len": cfg.ny,
+         "K": cfg.K, "Lf": cfg.lf, "nnz": cfg.nnz}
+    if wl in ("cfg1", "cfg2"):
+        d["out_len"] = cfg.ny + cfg.M - 1
+    d["sample"] = sample
+    return d
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
@@ -345,7 +357,7 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE laws)",
-        "config": {"workload": wl, "sample": desc},
+        "config": _workload_config(wl, desc),
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind, "sample": desc,
                          "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

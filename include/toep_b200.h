@@ -20,6 +20,12 @@
  *
  * Arithmetic is fp32 with fp32 accumulation (the reference computes in fp64);
  * parity target: relative L2 error <= 1e-5 against the reference.
+ *
+ * Threading (as the reference's plans and renderers, engine/__init__.py:16-18):
+ * distinct objects may be used concurrently from any thread / stream; the
+ * calls on one renderer, mixer or streamer must be ordered (one stream at a
+ * time) -- they own device scratch (check flag, tensor-map cache, the mix
+ * item counter, the stream history).  Read-only queries are always safe.
  */
 #ifndef TOEP_B200_H
 #define TOEP_B200_H

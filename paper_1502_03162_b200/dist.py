@@ -29,28 +29,39 @@ def partition(n_src: int, world: int, rank: int):
     return s0, base + (1 if rank < extra else 0)
 
 
-def partition_by_direction(src_dir, world: int):
+# cost of a rank's share of the mix, in units of one source's load work: each
+# source is read once; each distinct direction adds one tap pass over the
+# z samples (2 ears x nnz taps), measured on B200 at ~1.6 source loads
+# (cfg5: ~10 ms of loads for 4,096 sources against ~4.7 ms of taps for 1,204
+# directions, DESIGN.md section 7 attribution runs)
+DIRECTION_COST = 1.6
+
+
+def partition_by_direction(src_dir, world: int, direction_cost: float = DIRECTION_COST):
     """Per-rank source index lists (ascending) such that every direction's
-    sources land on one rank and the ranks hold balanced source counts: the
-    direction-sorted source list is cut into ``world`` runs of ~S/world
-    sources, each cut moved to the nearest direction boundary."""
+    sources land on one rank and the ranks carry balanced mix work: the
+    direction-sorted source list is cut at the direction boundaries nearest
+    to equal shares of (sources + direction_cost x distinct directions)."""
     sd = np.asarray(src_dir, dtype=np.int64)
     if world < 1:
         raise DataError("bad world size")
     order = np.argsort(sd, kind="stable")
-    ds = sd[order]
-    S = sd.size
-    cuts = [0]
+    if sd.size == 0:
+        return [order[:0] for _ in range(world)]
+    _, starts, counts = np.unique(sd[order], return_index=True, return_counts=True)
+    cum = np.cumsum(counts + float(direction_cost))  # work up to and including direction k
+    total = float(cum[-1])
+    bounds = [0]  # cut positions in directions
     for r in range(1, world):
-        c = int(round(r * S / world))
-        c = max(c, cuts[-1])
-        if 0 < c < S and ds[c] == ds[c - 1]:  # snap to the nearer direction boundary
-            lo = int(np.searchsorted(ds, ds[c], side="left"))
-            hi = int(np.searchsorted(ds, ds[c], side="right"))
-            c = lo if (c - lo) <= (hi - c) and lo >= cuts[-1] else hi
-        cuts.append(min(c, S))
-    cuts.append(S)
-    return [np.sort(order[cuts[r]:cuts[r + 1]]) for r in range(world)]
+        target = r * total / world
+        k = int(np.searchsorted(cum, target))  # first direction whose prefix reaches the target
+        # cut before k or after k, whichever lands nearer the target
+        before = cum[k - 1] if k > 0 else 0.0
+        k = k if (k < cum.size and abs(before - target) <= abs(cum[k] - target)) else min(k + 1, cum.size)
+        bounds.append(max(k, bounds[-1]))
+    bounds.append(cum.size)
+    pos = np.append(starts, sd.size)  # source position of each direction boundary
+    return [np.sort(order[pos[bounds[r]]:pos[bounds[r + 1]]]) for r in range(world)]
 
 
 def reduce_partials(z, dst: int = 0, group=None):

@@ -158,8 +158,9 @@ class TestSynthAndPartition:
 
 
 def test_partition_by_direction():
-    """Every direction's sources on one rank, balanced source counts, and each
-    rank touching ~1/N of the directions (the mix's tap work)."""
+    """Every direction's sources on one rank, balanced mix work (sources +
+    DIRECTION_COST x distinct directions), each rank touching ~1/N of the
+    directions (the mix's tap work)."""
     sd = synth.source_directions(4096, 1250, seed=5)
     for world in (1, 2, 3, 8):
         parts = tdist.partition_by_direction(sd, world)
@@ -167,9 +168,11 @@ def test_partition_by_direction():
         allidx = np.concatenate(parts)
         assert sorted(allidx.tolist()) == list(range(4096))
         dirs = [set(sd[p].tolist()) for p in parts]
+        cost = [len(p) + tdist.DIRECTION_COST * len(d) for p, d in zip(parts, dirs)]
         for i in range(world):
             assert all(not (dirs[i] & dirs[j]) for j in range(i + 1, world))
-            assert abs(len(parts[i]) - 4096 / world) <= 16
+            assert abs(len(parts[i]) - 4096 / world) <= 0.05 * 4096 / world + 8
+            assert abs(cost[i] - sum(cost) / world) <= 0.01 * sum(cost) / world + 8
         assert max(len(d) for d in dirs) <= 1.2 * len(set(sd.tolist())) / world
     sd2 = np.zeros(10, np.int32)  # one direction: everything on one rank
     parts = tdist.partition_by_direction(sd2, 4)

@@ -36,8 +36,6 @@ def main():
     for world in (1, args.world):
         parts = tdist.partition_by_direction(sd, world)
         for r, mine in enumerate(parts):
-            if world > 1 and r >= 2 and r != world - 1:
-                continue  # first two and last share are representative
             y = synth.device_sources(int(mine.size), cfg.ny, seed=1000 + r)
             mix = batch.MixRenderer(ms, sd[mine], cfg.ny)
             z = mix.alloc_z()

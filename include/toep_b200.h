@@ -147,6 +147,14 @@ int64_t toep_mixer_out_len(const toep_mixer* m); /* T + lf + length - 2 */
  * y: source s at y + (s - s0) * y_pitch. */
 int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s0, int32_t count, float* z,
                        int64_t z_pitch, void* stream);
+/* Kernel toep_mixer_partial uses: TOEP_PATH_TENSOR (split-fp16 GEMM over
+ * direction sums on the tensor cores, then an overlap-add; the default when
+ * ears x round_up(length, 8) <= 208) or TOEP_PATH_WINDOW (TMEM window + FFMA2
+ * per tap; TOEP_MIX_MMA=0 in the environment forces it). */
+int toep_mixer_path(const toep_mixer* m);
+/* Kernel launches per toep_mixer_partial call (tensor path: main pass, tile
+ * scan, fixup pass for tiles outside the fp16-safe range, overhang carry). */
+int toep_mixer_kernels(const toep_mixer* m);
 /* out[e] = f_e * z[e] (length out_len). */
 int toep_mixer_finish(const toep_mixer* m, const float* z, int64_t z_pitch, float* out, int64_t out_pitch,
                       void* stream);

@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 BUILD = os.path.join(PKG_DIR, "build")
 LIB_NAME = "libtoep_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
-SOURCES = ("render.cu", "render_mma.cu", "fir_mix.cu", "fft.cu", "capi.cu")
+SOURCES = ("render.cu", "render_mma.cu", "fir_mix.cu", "mix_mma.cu", "fft.cu", "capi.cu")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -27,7 +27,7 @@ EXPORTS = (
     "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check", "toep_renderer_path",
     "toep_renderer_kernels",
     "toep_mixer_create", "toep_mixer_destroy", "toep_mixer_z_len", "toep_mixer_out_len",
-    "toep_mixer_partial", "toep_mixer_finish",
+    "toep_mixer_partial", "toep_mixer_finish", "toep_mixer_path", "toep_mixer_kernels",
     "toep_streamer_create", "toep_streamer_destroy", "toep_streamer_reset", "toep_streamer_step",
 )
 
@@ -88,6 +88,8 @@ def load_library(path: str = LIB_PATH):
         "toep_mixer_out_len": (_i64, [_vp]),
         "toep_mixer_partial": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _vp, _i64, _vp]),
         "toep_mixer_finish": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
+        "toep_mixer_path": (ctypes.c_int, [_vp]),
+        "toep_mixer_kernels": (ctypes.c_int, [_vp]),
         "toep_streamer_create": (ctypes.c_int, [_vp, _i32p, _i32, _i32, ctypes.POINTER(_vp)]),
         "toep_streamer_destroy": (ctypes.c_int, [_vp]),
         "toep_streamer_reset": (ctypes.c_int, [_vp, _vp]),
@@ -274,6 +276,12 @@ class NativeMixer:
 
     def out_len(self) -> int:
         return int(load_library().toep_mixer_out_len(self._h))
+
+    def path(self) -> str:
+        return {1: "tensor", 0: "window"}[int(load_library().toep_mixer_path(self._h))]
+
+    def kernels(self) -> int:
+        return int(load_library().toep_mixer_kernels(self._h))
 
     def partial(self, y, y_pitch: int, s0: int, count: int, z, z_pitch: int, stream=None):
         check(load_library().toep_mixer_partial(self._h, dptr(y), int(y_pitch), int(s0), int(count), dptr(z),

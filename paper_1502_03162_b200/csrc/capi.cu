@@ -10,6 +10,8 @@
 #include <new>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "../../include/toep_b200.h"
 #include "launch.h"
 
@@ -713,7 +715,162 @@ struct toep_mixer {
   unsigned long long* d_work = nullptr;  // k_mix item counter
   float* d_part = nullptr;
   size_t part_bytes = 0;
+  // tensor-core path (mix_mma.cu): plan for the source range [mma_s0, mma_s0 + mma_count)
+  bool mma = false;
+  int N = 0, KP = 0, sexp = 20;
+  int mma_s0 = -1, mma_count = -1, KS = 0, n_tiles = 0, ovh_pitch = 0;
+  int* d_msrc = nullptr;
+  int2* d_mks = nullptr;
+  int* d_mrows = nullptr;
+  unsigned char* d_mg = nullptr;
+  float* d_ovh = nullptr;
+  float* d_tmax = nullptr;
+  int* d_bad = nullptr;  // [n_tiles] list + count
+  std::vector<int2> h_taps;  // [rows][tap_stride] {offset, value bits}
+  std::vector<int> h_nnz;
+  const float* map_y = nullptr;  // source tensor map of the last call
+  long long map_pitch = -1, map_rows = -1;
+  CUtensorMap map{};
 };
+
+// TOEP_MIX_MMA=0 selects the FFMA/TMEM-window mix kernel (A/B runs)
+static bool mix_mma_enabled() {
+  const char* ev = getenv("TOEP_MIX_MMA");
+  return !(ev && atoi(ev) == 0);
+}
+
+static void mma_plan_free(toep_mixer* m) {
+  for (void* p : {(void*)m->d_msrc, (void*)m->d_mks, (void*)m->d_mrows, (void*)m->d_mg, (void*)m->d_ovh,
+                  (void*)m->d_tmax, (void*)m->d_bad})
+    if (p) cudaFree(p);
+  m->d_msrc = nullptr;
+  m->d_mks = nullptr;
+  m->d_mrows = nullptr;
+  m->d_mg = nullptr;
+  m->d_ovh = nullptr;
+  m->d_tmax = nullptr;
+  m->d_bad = nullptr;
+  m->mma_s0 = m->mma_count = -1;
+}
+
+static inline int mma_canon_host(int r, int k, int R) {
+  return (k >> 4) * (R * 32) + (r >> 3) * 256 + ((k >> 3) & 1) * 128 + (r & 7) * 16 + (k & 7) * 2;
+}
+
+// K-step plan of the tensor-core mix for sources [s0, s0+count): sources sorted
+// by direction; a row = up to kMixRowSrcs sources of one direction; a K-step =
+// up to 16 rows and kMixKsSrcs sources; G columns scaled per direction by
+// 2^gamma_d (max |g_d| * 2^gamma_d in [2^13, 2^14)).
+static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
+  const toep_renderer* r = m->r;
+  const toep_taps* g = r->g;
+  if (m->h_taps.empty()) {
+    m->h_taps.resize((size_t)g->rows * g->tap_stride);
+    m->h_nnz.resize(g->rows);
+    TOEP_CUDA(cudaMemcpyAsync(m->h_taps.data(), g->d_raw, m->h_taps.size() * sizeof(int2), cudaMemcpyDeviceToHost, st));
+    TOEP_CUDA(cudaMemcpyAsync(m->h_nnz.data(), g->d_nnz, g->rows * sizeof(int), cudaMemcpyDeviceToHost, st));
+    TOEP_CUDA(cudaStreamSynchronize(st));
+  }
+  mma_plan_free(m);
+  const int* dir = m->h_dir.data() + s0;
+  std::vector<int> ord(count);
+  for (int i = 0; i < count; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
+  struct Row { int d, first, cnt; };
+  std::vector<Row> rows;
+  for (int p = 0; p < count;) {
+    int q = p;
+    while (q < count && dir[ord[q]] == dir[ord[p]]) ++q;
+    for (int a = p; a < q; a += kMixRowSrcs) rows.push_back({dir[ord[p]], a, std::min(kMixRowSrcs, q - a)});
+    p = q;
+  }
+  std::vector<int2> ks;
+  std::vector<int> rinfo;    // [KS][16] offset | count << 6 | (gamma_d + 128) << 9
+  std::vector<int> ks_dirs;  // [KS][16] direction per row (-1 empty), gamma_d
+  std::vector<int> src;      // K-step source lists, each padded to a multiple of 4 with an out-of-range row
+  for (size_t i = 0; i < rows.size();) {
+    const int start = rows[i].first;
+    int nr = 0, ns = 0;
+    while (i + nr < rows.size() && nr < 16 && ns + rows[i + nr].cnt <= kMixKsSrcs) ns += rows[i + nr++].cnt;
+    const int ns4 = (ns + 3) & ~3;
+    ks.push_back(make_int2((int)src.size(), ns4));
+    for (int k = 0; k < ns4; ++k) src.push_back(k < ns ? ord[start + k] : count);
+    for (int k = 0; k < 16; ++k) {
+      if (k < nr) {
+        const Row& w = rows[i + k];
+        float mx = 0.f;
+        for (int e = 0; e < r->ears; ++e) {
+          const int row = e * r->dirs + w.d;
+          for (int t = 0; t < m->h_nnz[row]; ++t) {
+            float v;
+            memcpy(&v, &m->h_taps[(size_t)row * g->tap_stride + t].y, 4);
+            mx = std::max(mx, std::fabs(v));
+          }
+        }
+        int gam = mx > 0.f ? 13 - std::ilogb(mx) : 0;
+        gam = std::max(-126, std::min(126, gam));
+        rinfo.push_back((w.first - start) | (w.cnt << 6) | ((gam + 128) << 9));
+        ks_dirs.push_back(w.d);
+        ks_dirs.push_back(gam);
+      } else {
+        rinfo.push_back(128 << 9);  // empty row (multiplier 2^0)
+        ks_dirs.push_back(-1);
+        ks_dirs.push_back(0);
+      }
+    }
+    i += nr;
+  }
+  const int KS = (int)ks.size();
+  const int N = m->N, KP = m->KP;
+  const size_t gb = (size_t)N * 64;
+  std::vector<unsigned char> G((size_t)KS * gb, 0);
+  for (int k = 0; k < KS; ++k) {
+    unsigned char* hi = G.data() + k * gb;
+    unsigned char* lo = hi + gb / 2;
+    for (int slot = 0; slot < 16; ++slot) {
+      const int d = ks_dirs[(k * 16 + slot) * 2], gam = ks_dirs[(k * 16 + slot) * 2 + 1];
+      if (d < 0) continue;
+      for (int e = 0; e < r->ears; ++e) {
+        const int row = e * r->dirs + d;
+        for (int t = 0; t < m->h_nnz[row]; ++t) {
+          const int2 tv = m->h_taps[(size_t)row * g->tap_stride + t];
+          float v;
+          memcpy(&v, &tv.y, 4);
+          const float x = std::ldexp(v, gam);
+          const __half h = __float2half_rn(x);
+          const __half l = __float2half_rn(x - __half2float(h));
+          const int off = mma_canon_host(e * KP + tv.x, slot, N);
+          memcpy(hi + off, &h, 2);
+          memcpy(lo + off, &l, 2);
+        }
+      }
+    }
+  }
+  m->KS = KS;
+  m->n_tiles = (int)((m->T + kMixTile - 1) / kMixTile);
+  m->ovh_pitch = (int)std::max<long long>(4, round_up(g->length - 1, 4));
+  cudaError_t e = cudaMalloc(&m->d_msrc, src.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_mks, KS * sizeof(int2));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_mrows, rinfo.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_mg, G.size());
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_ovh, (size_t)m->n_tiles * r->ears * m->ovh_pitch * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_tmax, (size_t)m->n_tiles * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_bad, (size_t)(m->n_tiles + 1) * sizeof(int));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(m->d_msrc, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->d_mks, ks.data(), KS * sizeof(int2), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(m->d_mrows, rinfo.data(), rinfo.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->d_mg, G.data(), G.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host staging vectors die here
+  if (e != cudaSuccess) {
+    mma_plan_free(m);
+    return cuda_fail(e, "mixer tensor-core plan");
+  }
+  m->mma_s0 = s0;
+  m->mma_count = count;
+  return TOEP_OK;
+}
 
 static cudaError_t ensure_part(toep_mixer* m, size_t need, cudaStream_t st) {
   if (need <= m->part_bytes) return cudaSuccess;
@@ -750,6 +907,15 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
   m->T = T;
   m->zlen = T + r->g->length - 1;
   m->h_dir.assign(src_dir_host, src_dir_host + n_src);
+  {
+    const int K = r->g->length;
+    m->KP = (int)round_up(K, 8);
+    m->N = (int)round_up((long long)r->ears * m->KP, 16);
+    const int ch = (K + 15) / 16, nr = (32 + K - 1 + 31) / 32;
+    m->mma = mix_mma_enabled() && m->N <= 208 && ((ch <= 7 && nr <= 5) || (ch <= 13 && nr <= 8));
+    const char* se = getenv("TOEP_MIX_SEXP");
+    if (se) m->sexp = std::max(-100, std::min(100, atoi(se)));
+  }
   cudaError_t e = cudaMalloc(&m->d_bsrc, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bptr, (n_src + 1) * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bdir, n_src * sizeof(int));
@@ -769,11 +935,14 @@ int toep_mixer_destroy(toep_mixer* m) {
   if (m->d_bdir) cudaFree(m->d_bdir);
   if (m->d_work) cudaFree(m->d_work);
   if (m->d_part) cudaFree(m->d_part);
+  mma_plan_free(m);
   delete m;
   return TOEP_OK;
 }
 
 int64_t toep_mixer_z_len(const toep_mixer* m) { return m ? m->zlen : -1; }
+int toep_mixer_path(const toep_mixer* m) { return m ? (m->mma ? TOEP_PATH_TENSOR : TOEP_PATH_WINDOW) : -1; }
+int toep_mixer_kernels(const toep_mixer* m) { return m ? (m->mma ? 4 : 3) : -1; }
 int64_t toep_mixer_out_len(const toep_mixer* m) { return m ? m->zlen + m->r->lf - 1 : -1; }
 
 int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s0, int32_t count, float* z,
@@ -787,6 +956,47 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   if (m->r->ears > 1 && z_pitch < m->zlen) return fail(TOEP_ERR_INVALID, "z pitch too small");
   cudaStream_t st = S(stream);
   const toep_taps* g = m->r->g;
+  if (m->mma) {
+    if (s0 != m->mma_s0 || count != m->mma_count) {
+      const int rc = mma_plan(m, s0, count, st);
+      if (rc != TOEP_OK) return rc;
+    }
+    MixMmaArgs a{};
+    a.y = y;
+    a.T = m->T;
+    a.y_pitch = count > 1 ? y_pitch : round_up(m->T, 4);
+    if (m->map_y != y || m->map_pitch != a.y_pitch || m->map_rows != count) {
+      cudaError_t em = make_mix_source_map(y, m->T, count, a.y_pitch, &m->map);
+      if (em != cudaSuccess) {
+        m->map_y = nullptr;
+        return cuda_fail(em, "tensor map (sources)");
+      }
+      m->map_y = y;
+      m->map_pitch = a.y_pitch;
+      m->map_rows = count;
+    }
+    a.src = m->d_msrc;
+    a.ks = m->d_mks;
+    a.rows = m->d_mrows;
+    a.g = m->d_mg;
+    a.KS = m->KS;
+    a.N = m->N;
+    a.KP = m->KP;
+    a.K = g->length;
+    a.ears = m->r->ears;
+    a.n_tiles = m->n_tiles;
+    a.sexp = m->sexp;
+    a.z = z;
+    a.z_pitch = m->r->ears > 1 ? z_pitch : 0;
+    a.zlen = m->zlen;
+    a.ovh = m->d_ovh;
+    a.ovh_pitch = m->ovh_pitch;
+    a.tile_max = m->d_tmax;
+    a.nonfinite = m->r->d_nonfinite;
+    cudaError_t e = launch_mix_mma(a, m->map, m->d_bad, m->d_bad + m->n_tiles, sm_count_cached(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_mix_mma");
+    return TOEP_OK;
+  }
   if (s0 != m->order_s0 || count != m->order_count) {
     // buckets: stable sort of the range by direction; bucket b = sources
     // bsrc[bptr[b] .. bptr[b+1]) (indices relative to s0), all at bdir[b]

@@ -179,6 +179,46 @@ cudaError_t launch_mix(const MixArgs& a, int kwin, int nnz_uniform, int sm_count
 cudaError_t launch_ear_pair_taps(const int2* rows, int dirs, int ears, int stride, int kwin, int4* out,
                                  cudaStream_t st);
 
+// Tensor-core mixdown (mix_mma.cu): W[t][(e,o)] = sum_d Y_d[t] G[d][(e,o)] on
+// tcgen05 (M = 128 time rows, K = 16 direction rows per step, N = ears x KP),
+// then z_e[t] = sum_o W[t-o][(e,o)].  The host plans K-steps of up to 16 rows
+// (a row = up to kMixRowSrcs sources of one direction, <= kMixKsSrcs per step).
+constexpr int kMixTile = 256;     // samples per tile (two 128-row blocks)
+constexpr int kMixRing = 160;     // 1 KB source slices in the shared-memory ring
+constexpr int kMixRowSrcs = 4;    // sources per direction row
+constexpr int kMixKsSrcs = 64;    // sources per K-step
+struct MixMmaArgs {
+  const float* y;        // sources, row i at y + i * y_pitch (16-byte aligned rows), length T
+  long long T;
+  long long y_pitch;
+  const int* src;        // source rows in K-step order, each K-step padded to a multiple of 4 (tensor-map rows)
+  const int2* ks;        // [KS] {first entry in src (multiple of 4), padded count}
+  const int* rows;       // [KS][16] row r: offset | count << 6 | (gamma_d + 128) << 9
+  const unsigned char* g;  // [KS][hi, lo][canonical N x 16] fp16 of g * 2^gamma_d
+  int KS;
+  int N;                 // MMA N (multiple of 16, <= 208)
+  int KP;                // columns per ear (K rounded up to 8)
+  int K;                 // reflection length
+  int ears;
+  int n_tiles;           // ceil(T / kMixTile)
+  int sexp;              // launch scale 2^sexp of the A operand
+  float* z;              // [ears][z_pitch], z_len = T + K - 1
+  long long z_pitch;
+  long long zlen;
+  float* ovh;            // [n_tiles][ears][ovh_pitch] overlap-add tails
+  int ovh_pitch;
+  float* tile_max;       // [n_tiles] max |Y_d 2^-gamma_d| per tile
+  const int* bad_list;   // fixup pass: tiles to re-render (null: every tile)
+  const int* bad_count;
+  int* nonfinite;
+};
+// main pass, bad-tile scan, fixup pass, overhang carry (4 launches)
+// tm: 2-D tensor map over the sources {T, rows}, box {kMixTile, 1} (tile::gather4 loads)
+cudaError_t launch_mix_mma(const MixMmaArgs& a, const CUtensorMap& tm, int* bad_list, int* bad_count, int sm_count,
+                           cudaStream_t st);
+cudaError_t make_mix_source_map(const float* y, long long T, long long rows, long long pitch, CUtensorMap* m);
+size_t mix_mma_smem(int N, int ears, int K);
+
 // z[e][t] = sum_g part[g][e][t]  (fixed order, fp32)
 cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long part_pitch, long long zlen,
                               float* z, long long z_pitch, cudaStream_t st);

@@ -1,0 +1,603 @@
+// Tensor-core mixdown (configs 4 offline and 5): the g-first partial mix
+//   z_e[t] = sum_s (y_s * g_{e,dir(s)})[t]
+// of many sources, each at one direction, as a GEMM on the tcgen05 tensor
+// cores followed by an overlap-add.
+//
+// Reference semantics: the sum over sources of toepnmf's Renderer.render
+// (pkg/src/toepnmf/engine/__init__.py:238-260 = conv_dense then conv_sparse,
+// engine/_kernels.pyx:11-44), reordered reflection-first by the associativity
+// the paper factorizes for (pkg/tests/test_acceptance.py:283-300);
+// the resonance f_e is applied once to z afterwards (k_fir).
+//
+// Formulation.  Sources sharing a direction are summed first (Y_d = sum y_s).
+// With n = (e, o) the output column for ear e and tap offset o,
+//     W[t][n] = sum_d Y_d[t] * G[d][n],   G[d][(e,o)] = g_{e,d}[o]
+//     z_e[t]  = sum_o W[t - o][(e,o)]                       (overlap-add)
+// The first line is a dense GEMM with M = time, K = directions, N = ears x
+// taps (2 x 104 = 208 at K = 100): the zero taps of the sparse g cost tensor
+// work, which has headroom -- the kernel is bound by the one read of every
+// source sample from HBM (4 B per source sample, 47 GB at config 5).  The
+// W formulation needs no halo on the loads: a tile of 256 samples reads
+// exactly samples [t0, t0+256) of each source; the (K-1)-sample tail of its
+// overlap-add ("overhang") is kept per tile and added by k_mix_carry.
+//
+// fp32 accuracy from fp16 operands as in render_mma.cu: x = hi + lo,
+// products hi*hi + hi*lo + lo*hi into fp32 TMEM accumulators.  G columns are
+// normalised per direction by 2^gamma_d (host); the A value of row d is
+// Y_d * 2^-gamma_d * 2^sexp (exact power-of-two scaling, undone in the
+// epilogue).  The launch scale 2^sexp is fixed per mixer; every tile records
+// max |Y_d 2^-gamma_d| and k_mix_scan lists the tiles whose values left the
+// fp16-safe window (overflow, or so small that the low half loses bits while
+// the tile still matters); a second launch of this kernel re-renders exactly
+// those tiles with their own scale.  Results are a deterministic function of
+// the input.
+//
+// Persistent CTA per SM (20 warps), tile = 256 samples = two 128-row blocks:
+//   warp 0      source producer: one 1 KB cp.async.bulk per (source, tile)
+//               into a ring of 1 KB slots (measured 7.06 TB/s for this
+//               pattern, tools/microbench/gather_rate.cu); a K-step's slices
+//               complete on one mbarrier
+//   warp 1      G producer: the K-step's G (hi, lo; canonical K-major
+//               SWIZZLE_NONE, 13 KB at N = 208) into a 3-stage ring
+//   warp 2      MMA issuer: per K-step 2 row blocks x 3 products of
+//               tcgen05.mma M=128 N=208 K=16 (A from TMEM, G from smem)
+//   warps 4-11  A builders (lane = time): per K-step sum each row's <= 4
+//               source slices (direction rows), scale, split hi/lo, tcgen05.st
+//               into a 3-slot TMEM ring
+//   warps 12-19 epilogue: tcgen05.ld of W, overlap-add through warp
+//               shuffles into per-lane registers, combine of the 8 warps'
+//               windows in shared memory, z stores + overhang
+// TMEM: accumulators [0, 2N), A slots [416, 512) (32 columns each: row block
+// 0 hi/lo, row block 1 hi/lo).
+#include <algorithm>
+#include <cstdio>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace toep {
+
+constexpr int kMxBuildWarps = 16;  // 4 per TMEM lane quarter: (row block, half of the K-step's 16 rows)
+constexpr int kMxEpiWarps = 4;     // one per lane quarter, both row blocks
+constexpr int kMxWarps = 4 + kMxBuildWarps + kMxEpiWarps;
+constexpr int kMxThreads = 32 * kMxWarps;
+constexpr int kMxKR = 16;      // K-step barrier ring
+constexpr int kMxGR = 3;       // G stages
+constexpr int kMxAR = 3;       // A slots in TMEM
+constexpr int kMxACol = 416;   // first A-slot column
+constexpr int kMxSlotBytes = kMixTile * 4;
+constexpr int kMxWindows = 8;  // overlap-add windows per tile: (row block, lane quarter)
+
+__device__ __forceinline__ uint64_t mx_sdesc(unsigned saddr) {
+  // canonical K-major, SWIZZLE_NONE: LBO (K halves) 128 B, SBO (8-row groups) 256 B, version 1
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void mx_mma(unsigned d_tmem, unsigned a_tmem, uint64_t db, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mx_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mx_st4(unsigned ta, unsigned a0, unsigned a1, unsigned a2, unsigned a3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "r"(a0), "r"(a1), "r"(a2),
+               "r"(a3)
+               : "memory");
+}
+// four source rows (tensor-map rows r0..r3, columns [col, col + 256)) -> 4 consecutive 1 KB slots
+__device__ __forceinline__ void mx_gather4(void* sdst, const CUtensorMap* tm, int col, int4 r, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(smem_u32(sdst)),
+      "l"(tm), "r"(col), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ unsigned mx_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);  // a -> low half (column element 2j), b -> high half
+  return *reinterpret_cast<const unsigned*>(&h);
+}
+__device__ __forceinline__ float p2f(int e) { return __int_as_float((127 + e) << 23); }  // 2^e, e in [-126, 127]
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+struct MxSmem {
+  int ring, g, ebuf, misc, bars, total;
+};
+__host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr) {
+  MxSmem L{};
+  L.ring = 0;
+  int off = kMixRing * kMxSlotBytes;
+  L.g = off;  // [kMxGR][hi, lo][N x 16] fp16
+  off += kMxGR * N * 64;
+  L.ebuf = off;  // [2][kMxWindows][ears][32 * nr] fp32
+  off += 2 * kMxWindows * ears * 32 * nr * 4;
+  L.misc = off;  // builder max per warp [16]
+  off += 64;
+  L.bars = off;
+  off += (2 * kMxKR + 2 * kMxGR + 2 * kMxAR + 2) * 8;
+  L.total = off;
+  return L;
+}
+
+// tile sequence of this CTA: a contiguous range (main pass) or its share of
+// the bad-tile list (fixup pass)
+struct MxTiles {
+  const int* list;
+  int j0, j1, cnt;
+  __device__ int at(int i) const {
+    if (!list) return j0 + i < j1 ? j0 + i : -1;
+    const int k = i * (int)gridDim.x + (int)blockIdx.x;
+    return k < cnt ? list[k] : -1;
+  }
+};
+
+__device__ __forceinline__ int mx_tile_sexp(const MixMmaArgs& a, int j) {
+  if (!a.bad_list) return a.sexp;
+  const float m = a.tile_max[j];  // unscaled max |Y_d 2^-gamma_d| of the tile
+  int s = m > 0.f ? 13 - ilogbf(m) : a.sexp;
+  return max(-100, min(100, s));
+}
+
+#ifndef TOEP_MIX_PROF
+#define TOEP_MIX_PROF 0
+#endif
+#if TOEP_MIX_PROF
+#define PROF_WAIT(slot, ...)         \
+  do {                               \
+    const long long _t0 = clock64(); \
+    __VA_ARGS__;                     \
+    prof[slot] += clock64() - _t0;   \
+  } while (0)
+#else
+#define PROF_WAIT(slot, ...) __VA_ARGS__
+#endif
+
+template <int CH, int NR>
+__global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw;
+  const int N = a.N;
+  const MxSmem L = mx_smem(N, a.ears, NR);
+  const int gbytes = N * 64;
+  float* ring = reinterpret_cast<float*>(sm + L.ring);
+  unsigned char* sG = sm + L.g;
+  float* ebuf = reinterpret_cast<float*>(sm + L.ebuf);
+  float* s_bmax = reinterpret_cast<float*>(sm + L.misc);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+  uint64_t* src_full = bars;
+  uint64_t* src_empty = src_full + kMxKR;
+  uint64_t* g_full = src_empty + kMxKR;
+  uint64_t* g_empty = g_full + kMxGR;
+  uint64_t* a_full = g_empty + kMxGR;
+  uint64_t* a_empty = a_full + kMxAR;
+  uint64_t* acc_full = a_empty + kMxAR;
+  uint64_t* acc_empty = acc_full + 1;
+  __shared__ unsigned s_tbase;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if TOEP_MIX_PROF
+  long long prof[4] = {0, 0, 0, 0};
+  const long long t_start = clock64();
+#endif
+
+  if (warp == 3) tmem_alloc<512>(&s_tbase);
+  if (tid == 0) {
+    for (int i = 0; i < kMxKR; ++i) {
+      mbar_init(&src_full[i], 1);
+      mbar_init(&src_empty[i], kMxBuildWarps);
+    }
+    for (int i = 0; i < kMxGR; ++i) {
+      mbar_init(&g_full[i], 1);
+      mbar_init(&g_empty[i], 1);
+    }
+    for (int i = 0; i < kMxAR; ++i) {
+      mbar_init(&a_full[i], kMxBuildWarps);
+      mbar_init(&a_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kMxEpiWarps);
+    mbar_fence_init();
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const unsigned tbase = s_tbase;
+
+  MxTiles tiles;
+  tiles.list = a.bad_list;
+  tiles.j0 = (int)((long long)a.n_tiles * blockIdx.x / gridDim.x);
+  tiles.j1 = (int)((long long)a.n_tiles * (blockIdx.x + 1) / gridDim.x);
+  tiles.cnt = a.bad_list ? *a.bad_count : 0;
+  const int KS = a.KS;
+
+  if (warp == 0) {
+    // ===== source producer: the K-step's source rows (padded to 4) as tile::gather4
+    //       tensor copies, lane g issuing gather g; next K-step's rows prefetched =====
+    long long seq = 0, fseq = 0;  // K-steps issued / released
+    int pos = 0;                  // next free slot (a K-step never wraps: its slots restart at 0)
+    int held = 0;                 // slots held by unreleased K-steps (incl. skipped tails)
+    int hold[kMxKR];              // slots each in-flight K-step holds
+    const int4* src4 = reinterpret_cast<const int4*>(a.src);
+    int2 info = __ldg(a.ks);
+    int4 nxt = lane < (info.y >> 2) ? __ldg(src4 + (info.x >> 2) + lane) : make_int4(0, 0, 0, 0);
+    for (int i = 0;; ++i) {
+      const int j = tiles.at(i);
+      if (j < 0) break;
+      const int col = j * kMixTile;
+      for (int ks = 0; ks < KS; ++ks) {
+        const int n = info.y;  // multiple of 4
+        const int4 cur = nxt;
+        info = __ldg(a.ks + (ks + 1 < KS ? ks + 1 : 0));
+        nxt = lane < (info.y >> 2) ? __ldg(src4 + (info.x >> 2) + lane) : make_int4(0, 0, 0, 0);
+        const int skip = pos + n > kMixRing ? kMixRing - pos : 0;
+        while (seq - fseq >= kMxKR || held + skip + n > kMixRing) {
+          PROF_WAIT(0, mbar_wait(&src_empty[fseq % kMxKR], (unsigned)((fseq / kMxKR) & 1)));
+          held -= hold[fseq % kMxKR];
+          ++fseq;
+        }
+        if (pos + n > kMixRing) pos = 0;
+        hold[seq % kMxKR] = skip + n;
+        held += skip + n;
+        uint64_t* bar = &src_full[seq % kMxKR];
+        if (lane == 0) mbar_arrive_expect_tx(bar, (unsigned)(n * kMxSlotBytes));
+        __syncwarp();
+        if (4 * lane < n) mx_gather4(ring + (pos + 4 * lane) * kMixTile, &tm, col, cur, bar);
+        pos += n;
+        ++seq;
+      }
+    }
+  } else if (warp == 1) {
+    // ===== G producer =====
+    if (elect_one()) {
+      int gs = 0;
+      unsigned gph = 0;
+      for (int i = 0;; ++i) {
+        if (tiles.at(i) < 0) break;
+        for (int ks = 0; ks < KS; ++ks) {
+          PROF_WAIT(0, mbar_wait_sleep(&g_empty[gs], gph ^ 1u));
+          mbar_arrive_expect_tx(&g_full[gs], (unsigned)gbytes);
+          bulk_load(sG + gs * gbytes, a.g + (long long)ks * gbytes, (unsigned)gbytes, &g_full[gs]);
+          if (++gs == kMxGR) {
+            gs = 0;
+            gph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ===== MMA issuer =====
+    if (elect_one()) {
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const unsigned sg = smem_u32(sG);
+      int gs = 0, as = 0;
+      unsigned gph = 0, aph = 0, cph = 0;
+      for (int i = 0;; ++i) {
+        if (tiles.at(i) < 0) break;
+        PROF_WAIT(2, mbar_wait_sleep(acc_empty, cph ^ 1u));  // the epilogue has drained the accumulators
+        tmem_fence_after();
+        for (int ks = 0; ks < KS; ++ks) {
+          PROF_WAIT(0, mbar_wait(&g_full[gs], gph));
+          PROF_WAIT(1, mbar_wait(&a_full[as], aph));
+          tmem_fence_after();
+          const unsigned bh = sg + (unsigned)(gs * gbytes), bl = bh + (unsigned)(N * 32);
+#pragma unroll
+          for (int rb = 0; rb < 2; ++rb) {
+            const unsigned d = tbase + (unsigned)(rb * N);
+            const unsigned ah = tbase + (unsigned)(kMxACol + 32 * as + 16 * rb), al = ah + 8;
+            mx_mma(d, ah, mx_sdesc(bh), idesc, ks > 0);
+            mx_mma(d, ah, mx_sdesc(bl), idesc, 1);
+            mx_mma(d, al, mx_sdesc(bh), idesc, 1);
+          }
+          mx_commit(&a_empty[as]);
+          mx_commit(&g_empty[gs]);
+          if (++gs == kMxGR) {
+            gs = 0;
+            gph ^= 1u;
+          }
+          if (++as == kMxAR) {
+            as = 0;
+            aph ^= 1u;
+          }
+        }
+        mx_commit(acc_full);
+        cph ^= 1u;
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + kMxBuildWarps) {
+    // ===== A builders: lane = time; 8 of the K-step's 16 direction rows (<= 4 slices each) =====
+    const int bw = warp - 4;
+    const int q = warp & 3, rb = (bw >> 2) & 1, half = bw >> 3;
+    const int tt = 128 * rb + 32 * q + lane;  // time within the tile
+    const unsigned ta0 = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(kMxACol + 16 * rb + 4 * half);
+    long long seq = 0;
+    int pos = 0, as = 0;
+    unsigned aph = 0;
+    float chk0 = 0.f, chk1 = 0.f;
+    // row info of the next K-step is loaded one K-step ahead (8 rows x 4 B = 2 int4)
+    const int4* rtab = reinterpret_cast<const int4*>(a.rows) + 2 * half;
+    int4 nr0 = __ldg(rtab), nr1 = __ldg(rtab + 1);
+    int nn = __ldg(&a.ks[0].y);
+    for (int i = 0;; ++i) {
+      const int j = tiles.at(i);
+      if (j < 0) break;
+      const long long t0 = (long long)j * kMixTile;
+      const bool valid = t0 + tt < a.T;
+      const int sexp = mx_tile_sexp(a, j);
+      const float S = p2f(sexp);
+      float amax = 0.f;
+      for (int ks = 0; ks < KS; ++ks) {
+        const int n = nn;
+        const int ri[8] = {nr0.x, nr0.y, nr0.z, nr0.w, nr1.x, nr1.y, nr1.z, nr1.w};
+        {
+          const int kn = ks + 1 < KS ? ks + 1 : 0;
+          nr0 = __ldg(rtab + 4 * kn);
+          nr1 = __ldg(rtab + 4 * kn + 1);
+          nn = __ldg(&a.ks[kn].y);
+        }
+        if (pos + n > kMixRing) pos = 0;
+        int off[8], cnt[8];
+        float mul[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          off[r] = ri[r] & 63;
+          cnt[r] = (ri[r] >> 6) & 7;
+          mul[r] = __int_as_float((255 - ((ri[r] >> 9) & 0xff)) << 23);  // 2^-gamma_d
+        }
+        PROF_WAIT(0, mbar_wait(&src_full[seq % kMxKR], (unsigned)((seq / kMxKR) & 1)));
+        const float* base = ring + pos * kMixTile + tt;
+        float v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float* p = base + off[r] * kMixTile;
+          float s0 = 0.f, s1 = 0.f;
+          if (cnt[r] > 0) s0 = p[0];
+          if (cnt[r] > 1) s1 = p[kMixTile];
+          if (cnt[r] > 2) s0 += p[2 * kMixTile];
+          if (cnt[r] > 3) s1 += p[3 * kMixTile];
+          v[r] = s0 + s1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&src_empty[seq % kMxKR]);
+        unsigned hw[4], lw[4];
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          float x0 = valid ? v[r] * mul[r] : 0.f;  // Y_d 2^-gamma_d
+          float x1 = valid ? v[r + 1] * mul[r + 1] : 0.f;
+          chk0 = fmaf(x0, 0.f, chk0);
+          chk1 = fmaf(x1, 0.f, chk1);
+          amax = fmaxf(amax, fmaxf(fabsf(x0), fabsf(x1)));
+          x0 *= S;
+          x1 *= S;
+          const unsigned h = mx_h2(x0, x1);
+          const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
+          hw[r / 2] = h;
+          lw[r / 2] = mx_h2(x0 - hf.x, x1 - hf.y);
+        }
+        PROF_WAIT(1, mbar_wait(&a_empty[as], aph ^ 1u));
+        tmem_fence_after();
+        const unsigned ta = ta0 + (unsigned)(32 * as);
+        mx_st4(ta, hw[0], hw[1], hw[2], hw[3]);
+        mx_st4(ta + 8, lw[0], lw[1], lw[2], lw[3]);
+        tmem_wait_st();
+        tmem_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[as]);
+        if (++as == kMxAR) {
+          as = 0;
+          aph ^= 1u;
+        }
+        pos += n;
+        ++seq;
+      }
+      if (!a.bad_list) {  // tile max (unscaled) for the fixup scan
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) s_bmax[bw] = amax;
+        named_sync(1, 32 * kMxBuildWarps);
+        if (bw == 0 && lane == 0) {
+          float m = 0.f;
+          for (int w = 0; w < kMxBuildWarps; ++w) m = fmaxf(m, s_bmax[w]);
+          a.tile_max[j] = m;
+        }
+        named_sync(1, 32 * kMxBuildWarps);
+      }
+    }
+    if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk0 + chk1)) && lane == 0) atomicOr(a.nonfinite, 1);
+  } else if (warp >= 4 + kMxBuildWarps) {
+    // ===== epilogue: W -> overlap-add -> z (one warp per lane quarter, both row blocks) =====
+    const int q = warp & 3;
+    const int ears = a.ears, K = a.K, KP = a.KP;
+    const int win = 32 * NR;
+    unsigned cph = 0;
+    for (int i = 0;; ++i) {
+      const int j = tiles.at(i);
+      if (j < 0) break;
+      float* eb = ebuf + ((i & 1) * kMxWindows * ears) * win;
+      PROF_WAIT(0, mbar_wait(acc_full, cph));
+      cph ^= 1u;
+      tmem_fence_after();
+#pragma unroll 1
+      for (int rb = 0; rb < 2; ++rb) {
+        const unsigned tq = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(rb * N);
+        float R0[NR], R1[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          R0[k] = 0.f;
+          R1[k] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          float w0[16], w1[16];
+          tmem_ld16(w0, tq + (unsigned)(16 * c));
+          if (ears > 1) tmem_ld16(w1, tq + (unsigned)(KP + 16 * c));
+          tmem_wait_ld();
+          if (rb == 1 && c == CH - 1) {  // every accumulator column this warp reads has been read
+            tmem_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+          }
+          // W[t][o] (lane t) belongs to window position t + o: lane L collects
+          // the positions = L (mod 32) from lane (L - o) mod 32
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int o = 16 * c + jj;
+            if (o < K) {
+              const int srcl = (lane - o) & 31;
+              const float x0 = __shfl_sync(0xffffffffu, w0[jj], srcl);
+              const float x1 = ears > 1 ? __shfl_sync(0xffffffffu, w1[jj], srcl) : 0.f;
+              const int kb = o >> 5;
+              if (srcl + (o & 31) < 32) {
+                R0[kb] += x0;
+                R1[kb] += x1;
+              } else if (kb + 1 < NR) {
+                R0[kb + 1] += x0;
+                R1[kb + 1] += x1;
+              }
+            }
+          }
+        }
+        const int w = 4 * rb + q;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          eb[(w * ears) * win + 32 * k + lane] = R0[k];
+          if (ears > 1) eb[(w * ears + 1) * win + 32 * k + lane] = R1[k];
+        }
+      }
+      named_sync(2, 32 * kMxEpiWarps);
+      // combine the 8 windows (fixed order): position P of the tile's 256 + K - 1
+      const long long t0 = (long long)j * kMixTile;
+      const float inv = p2f(-mx_tile_sexp(a, j));
+      const int npos = kMixTile + K - 1;
+      const int et = tid - 32 * (4 + kMxBuildWarps);
+      for (int idx = et; idx < ears * npos; idx += 32 * kMxEpiWarps) {
+        const int e = idx / npos, P = idx - e * npos;
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < kMxWindows; ++w) {
+          const int b = 128 * (w >> 2) + 32 * (w & 3);
+          if (P >= b && P < b + win) acc += eb[(w * ears + e) * win + (P - b)];
+        }
+        acc *= inv;
+        if (P < kMixTile) {
+          if (t0 + P < a.zlen) a.z[(long long)e * a.z_pitch + t0 + P] = acc;
+        } else {
+          a.ovh[((long long)j * ears + e) * a.ovh_pitch + (P - kMixTile)] = acc;
+        }
+      }
+    }
+  }
+#if TOEP_MIX_PROF
+  if (blockIdx.x == 0 && (warp <= 2 || warp == 4 || warp == 4 + kMxBuildWarps) &&
+      (lane == 0 || prof[0] + prof[1] + prof[2] > 0) && (warp != 0 || lane == 0))
+    printf("mixprof warp %d total %lld waits: %lld %lld %lld\n", warp, clock64() - t_start, prof[0], prof[1],
+           prof[2]);
+#endif
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 3) tmem_dealloc<512>(tbase);
+}
+
+// bad-tile list for the fixup pass (one CTA)
+__global__ void __launch_bounds__(1024) k_mix_scan(const float* __restrict__ tile_max, int n_tiles, int sexp,
+                                                    int* __restrict__ list, int* __restrict__ count) {
+  __shared__ float s_red[32];
+  float m = 0.f;
+  for (int j = threadIdx.x; j < n_tiles; j += blockDim.x) {
+    const float v = tile_max[j];
+    if (isfinite(v)) m = fmaxf(m, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+  if (threadIdx.x == 0) *count = 0;
+  __syncthreads();
+  float g = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) g = fmaxf(g, s_red[w]);
+  const float S = ldexpf(1.f, sexp);
+  for (int j = threadIdx.x; j < n_tiles; j += blockDim.x) {
+    const float v = tile_max[j];
+    if (!isfinite(v) || v == 0.f) continue;
+    const float s = v * S;
+    // fp16-safe window of the scaled tile: |x| <= 2^15 (no overflow of the
+    // hi half) and, for a tile that matters (>= 2^-24 of the loudest), >= 2^-3
+    // (the lo half stays a normal fp16 number for the tile's largest values)
+    const bool bad = s > 32768.f || (s < 0.125f && v >= g * 5.9604645e-8f);
+    if (bad) list[atomicAdd(count, 1)] = j;
+  }
+}
+
+// z[e][256 (j+1) + p] += ovh[j][e][p]  (the last tile's overhang is stored)
+__global__ void k_mix_carry(float* __restrict__ z, long long z_pitch, long long zlen, const float* __restrict__ ovh,
+                            int ovh_pitch, int n_tiles, int ears, int nov) {
+  const long long total = (long long)n_tiles * ears * nov;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int p = (int)(i % nov);
+    const long long je = i / nov;
+    const int e = (int)(je % ears);
+    const long long j = je / ears;
+    const long long pos = (j + 1) * kMixTile + p;
+    if (pos >= zlen) continue;
+    const float v = ovh[(j * ears + e) * ovh_pitch + p];
+    float* zp = z + (long long)e * z_pitch + pos;
+    *zp = (j + 1 < n_tiles ? *zp : 0.f) + v;
+  }
+}
+
+int mix_mma_nr(int K) { return (32 + K - 1 + 31) / 32; }
+
+size_t mix_mma_smem(int N, int ears, int K) {
+  const int nr = mix_mma_nr(K) <= 5 ? 5 : 8;
+  return (size_t)mx_smem(N, ears, nr).total;
+}
+
+template <int CH, int NR>
+static cudaError_t launch_mix_mma_t(const MixMmaArgs& a, const CUtensorMap& tm, int grid, cudaStream_t st) {
+  const int bytes = mx_smem(a.N, a.ears, NR).total;
+  auto kern = k_mix_mma<CH, NR>;
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), bytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kMxThreads, bytes, st>>>(a, tm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mix_mma(const MixMmaArgs& a_in, const CUtensorMap& tm, int* bad_list, int* bad_count,
+                           int sm_count, cudaStream_t st) {
+  if (a_in.N < 16 || a_in.N > 208 || a_in.N % 16 || a_in.K < 1) return cudaErrorInvalidValue;
+  const int nr = mix_mma_nr(a_in.K);
+  const int ch = (a_in.K + 15) / 16;
+  MixMmaArgs a = a_in;
+  a.bad_list = nullptr;
+  a.bad_count = nullptr;
+  const int grid = std::max(1, std::min(sm_count, a.n_tiles));
+  auto go = [&](const MixMmaArgs& x) -> cudaError_t {
+    if (ch <= 7 && nr <= 5) return launch_mix_mma_t<7, 5>(x, tm, grid, st);
+    if (ch <= 13 && nr <= 8) return launch_mix_mma_t<13, 8>(x, tm, grid, st);
+    return cudaErrorInvalidValue;
+  };
+  cudaError_t e = go(a);
+  if (e != cudaSuccess) return e;
+  k_mix_scan<<<1, 1024, 0, st>>>(a.tile_max, a.n_tiles, a.sexp, bad_list, bad_count);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  MixMmaArgs f = a;
+  f.bad_list = bad_list;
+  f.bad_count = bad_count;
+  f.nonfinite = nullptr;
+  e = go(f);
+  if (e != cudaSuccess) return e;
+  const int nov = a.K - 1;
+  if (nov > 0) {
+    const long long total = (long long)a.n_tiles * a.ears * nov;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sm_count * 8);
+    k_mix_carry<<<std::max(blocks, 1), 256, 0, st>>>(a.z, a.z_pitch, a.zlen, a.ovh, a.ovh_pitch, a.n_tiles, a.ears,
+                                                      nov);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace toep

@@ -518,6 +518,23 @@ cudaError_t make_render_mma_map(float* out, int ears, int dirs, long long out_le
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 2-D map over the mixer's source rows {T, rows} (row pitch `pitch` floats),
+// box {kMixTile, 1}: k_mix_mma loads 4 rows per tile::gather4; columns past T
+// and rows past `rows` (the K-step padding) are zero-filled by TMA.
+cudaError_t make_mix_source_map(const float* y, long long T, long long rows, long long pitch, CUtensorMap* m) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(y) & 15) || (pitch * 4) % 16) return cudaErrorInvalidValue;
+  const cuuint64_t dims[2] = {(cuuint64_t)T, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kMixTile, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(y), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 int render_kwin_for(int K) {
   if (K <= 113) return 112;
   if (K <= 241) return 240;

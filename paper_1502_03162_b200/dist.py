@@ -64,9 +64,10 @@ def partition_by_direction(src_dir, world: int, direction_cost: float = DIRECTIO
     modelled work (sources + direction_cost x distinct directions).  A cut is
     snapped to the nearest direction boundary -- so the direction's sources
     stay on one rank and its tap pass runs once -- unless snapping would move
-    the cut by more than a direction's own cost from its target; then (with
-    ``split``) the cut falls inside the direction and both ranks run its tap
-    pass on their part of its sources.  Deterministic in ``src_dir``."""
+    the cut by more than 2% of a rank's share (and more than a direction's
+    own cost) from its target; then (with ``split``) the cut falls inside the
+    direction and both ranks run its tap pass on their part of its sources.
+    Deterministic in ``src_dir``."""
     sd = np.asarray(src_dir, dtype=np.int64)
     world = int(world)
     if world < 1:
@@ -93,7 +94,7 @@ def partition_by_direction(src_dir, world: int, direction_cost: float = DIRECTIO
         cands = [bounds[j] for j in (k - 1, k) if 0 <= j < bounds.size]
         b = min(cands, key=lambda p: (abs(cum[p] - target), p))
         cut = int(b)
-        if split and abs(cum[b] - target) > direction_cost + 1.0:
+        if split and abs(cum[b] - target) > max(direction_cost + 1.0, 0.02 * total / world):
             # inside a direction: the first position whose prefix work reaches the target
             cut = int(min(S, np.searchsorted(cum, target)))
         cuts.append(max(cut, cuts[-1]))

@@ -104,3 +104,19 @@ def device_sources(S: int, T: int, seed: int = 0, device: str = "cuda", out=None
         out = torch.empty((S, T), device=device, dtype=torch.float32)
     out.normal_(generator=g)
     return out
+
+
+def device_sources_indexed(indices, T: int, seed: int = 0, device: str = "cuda", out=None):
+    """Rows of the global source set: row i holds source ``indices[i]`` drawn on
+    the device from its own Philox stream (seed, global index), so a sharded
+    run renders exactly the sources a one-GPU run renders."""
+    import torch
+
+    idx = np.asarray(indices, dtype=np.int64)
+    if out is None:
+        out = torch.empty((idx.size, T), device=device, dtype=torch.float32)
+    g = torch.Generator(device=device)
+    for i, s in enumerate(idx):
+        g.manual_seed(int(seed) * 1_000_003 + int(s))
+        out[i].normal_(generator=g)
+    return out

@@ -174,6 +174,8 @@ def test_partition_by_direction():
             assert abs(len(parts[i]) - 4096 / world) <= 0.05 * 4096 / world + 8
             assert abs(cost[i] - sum(cost) / world) <= 0.01 * sum(cost) / world + 8
         assert max(len(d) for d in dirs) <= 1.2 * len(set(sd.tolist())) / world
-    sd2 = np.zeros(10, np.int32)  # one direction: everything on one rank
-    parts = tdist.partition_by_direction(sd2, 4)
+    sd2 = np.zeros(10, np.int32)  # one direction: kept whole without splitting, split otherwise
+    parts = tdist.partition_by_direction(sd2, 4, split=False)
     assert sorted(len(p) for p in parts) == [0, 0, 0, 10]
+    parts = tdist.partition_by_direction(sd2, 4)
+    assert sorted(len(p) for p in parts) == [2, 2, 3, 3]

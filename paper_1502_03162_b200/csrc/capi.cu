@@ -450,7 +450,8 @@ struct toep_renderer {
   int* d_nonfinite = nullptr;  // sticky flag: a kernel read a non-finite input sample
   int4* d_epairs = nullptr;    // [dirs][tap_stride] ear-interleaved taps (mixdown)
   void* d_gmma = nullptr;      // tensor-core operand tables (render_mma.cu), null if unsupported
-  float* d_gscale = nullptr;   // [ears][chunks]
+  int* d_gexp = nullptr;       // [ears][chunks][129] G row exponents + wide flag
+  MmaFillStreams fill;         // this renderer's side stream for the concurrent fill launch
   // last output tensor map (encoding costs microseconds of host time per call)
   std::mutex map_mu;
   const float* map_out = nullptr;
@@ -504,10 +505,14 @@ int toep_renderer_create(const float* f_host, int32_t ears, int32_t lf, const to
     if (e == cudaSuccess && render_mma_supported(g->length, r->lf_pad)) {
       const int cn = render_mma_chunk(), nch = (dirs + cn - 1) / cn;
       e = cudaMalloc(&r->d_gmma, render_mma_gbytes(ears, dirs, g->length));
-      if (e == cudaSuccess) e = cudaMalloc(&r->d_gscale, (size_t)ears * nch * sizeof(float));
+      (void)nch;
+      if (e == cudaSuccess) e = cudaMalloc(&r->d_gexp, render_mma_gexp_ints(ears, dirs) * sizeof(int));
       if (e == cudaSuccess)
         e = build_render_mma_tables(g->d_raw, g->d_nnz, dirs, ears, g->tap_stride, g->length, r->d_gmma,
-                                    r->d_gscale, nullptr);
+                                    r->d_gexp, nullptr);
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->fill.side, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->fill.fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->fill.join, cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
@@ -525,7 +530,10 @@ int toep_renderer_destroy(toep_renderer* r) {
   if (r->d_nonfinite) cudaFree(r->d_nonfinite);
   if (r->d_epairs) cudaFree(r->d_epairs);
   if (r->d_gmma) cudaFree(r->d_gmma);
-  if (r->d_gscale) cudaFree(r->d_gscale);
+  if (r->d_gexp) cudaFree(r->d_gexp);
+  if (r->fill.side) cudaStreamDestroy(r->fill.side);
+  if (r->fill.fork) cudaEventDestroy(r->fill.fork);
+  if (r->fill.join) cudaEventDestroy(r->fill.join);
   if (r->d_pairs) cudaFree(r->d_pairs);
   if (r->d_pnnz) cudaFree(r->d_pnnz);
   delete r;
@@ -598,7 +606,7 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
     a.f = r->d_f;
     a.lf_pad = r->lf_pad;
     a.g = r->d_gmma;
-    a.gscale = r->d_gscale;
+    a.gexp = r->d_gexp;
     a.kpad = render_mma_kpad(g->length);
     a.nchunks = (r->dirs + render_mma_chunk() - 1) / render_mma_chunk();
     a.dirs = r->dirs;
@@ -625,7 +633,7 @@ int toep_renderer_render(const toep_renderer* r, const float* y, int64_t ny, flo
       }
       map = rm->map;
     }
-    cudaError_t e = launch_render_mma(a, map, sm_count_cached(), st);
+    cudaError_t e = launch_render_mma(a, map, r->fill, sm_count_cached(), st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_render_mma");
     return TOEP_OK;
   }
@@ -718,8 +726,8 @@ struct toep_mixer {
   // tensor-core path (mix_mma.cu): plan for the source range [mma_s0, mma_s0 + mma_count)
   bool mma = false;
   int N = 0, KP = 0, sexp = 20;
-  int mma_s0 = -1, mma_count = -1, KS = 0, n_tiles = 0, ovh_pitch = 0;
-  int* d_msrc = nullptr;
+  int mma_s0 = -1, mma_count = -1, KS = 0, n_tiles = 0, ovh_pitch = 0, nsrc4 = 0, ring = 0;
+  unsigned short* d_msrc = nullptr;
   int2* d_mks = nullptr;
   int* d_mrows = nullptr;
   unsigned char* d_mg = nullptr;
@@ -787,14 +795,14 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   std::vector<int2> ks;
   std::vector<int> rinfo;    // [KS][16] offset | count << 6 | (gamma_d + 128) << 9
   std::vector<int> ks_dirs;  // [KS][16] direction per row (-1 empty), gamma_d
-  std::vector<int> src;      // K-step source lists, each padded to a multiple of 4 with an out-of-range row
+  std::vector<unsigned short> src;  // K-step source lists, each padded to a multiple of 4 with an out-of-range row
   for (size_t i = 0; i < rows.size();) {
     const int start = rows[i].first;
     int nr = 0, ns = 0;
     while (i + nr < rows.size() && nr < 16 && ns + rows[i + nr].cnt <= kMixKsSrcs) ns += rows[i + nr++].cnt;
     const int ns4 = (ns + 3) & ~3;
     ks.push_back(make_int2((int)src.size(), ns4));
-    for (int k = 0; k < ns4; ++k) src.push_back(k < ns ? ord[start + k] : count);
+    for (int k = 0; k < ns4; ++k) src.push_back((unsigned short)(k < ns ? ord[start + k] : count));
     for (int k = 0; k < 16; ++k) {
       if (k < nr) {
         const Row& w = rows[i + k];
@@ -847,9 +855,15 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
     }
   }
   m->KS = KS;
+  m->nsrc4 = (int)src.size();
+  m->ring = mix_mma_ring(N, r->ears, g->length, m->nsrc4, KS);
+  if (m->ring == 0) {  // K-step tables too large for shared memory: take the FFMA mix
+    m->mma = false;
+    return TOEP_OK;
+  }
   m->n_tiles = (int)((m->T + kMixTile - 1) / kMixTile);
   m->ovh_pitch = (int)std::max<long long>(4, round_up(g->length - 1, 4));
-  cudaError_t e = cudaMalloc(&m->d_msrc, src.size() * sizeof(int));
+  cudaError_t e = cudaMalloc(&m->d_msrc, src.size() * sizeof(unsigned short));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mks, KS * sizeof(int2));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mrows, rinfo.size() * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mg, G.size());
@@ -857,7 +871,7 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   if (e == cudaSuccess) e = cudaMalloc(&m->d_tmax, (size_t)m->n_tiles * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_bad, (size_t)(m->n_tiles + 1) * sizeof(int));
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(m->d_msrc, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(m->d_msrc, src.data(), src.size() * sizeof(unsigned short), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(m->d_mks, ks.data(), KS * sizeof(int2), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(m->d_mrows, rinfo.data(), rinfo.size() * sizeof(int), cudaMemcpyHostToDevice, st);
@@ -912,7 +926,8 @@ int toep_mixer_create(const toep_renderer* r, const int32_t* src_dir_host, int32
     m->KP = (int)round_up(K, 8);
     m->N = (int)round_up((long long)r->ears * m->KP, 16);
     const int ch = (K + 15) / 16, nr = (32 + K - 1 + 31) / 32;
-    m->mma = mix_mma_enabled() && m->N <= 208 && ((ch <= 7 && nr <= 5) || (ch <= 13 && nr <= 8));
+    // overhang of one tile must stay within the next tile (K - 1 <= kMixTile)
+    m->mma = mix_mma_enabled() && m->N <= 208 && K - 1 <= kMixTile && ((ch <= 7 && nr <= 5) || (ch <= 13 && nr <= 8));
     const char* se = getenv("TOEP_MIX_SEXP");
     if (se) m->sexp = std::max(-100, std::min(100, atoi(se)));
   }
@@ -956,11 +971,12 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
   if (m->r->ears > 1 && z_pitch < m->zlen) return fail(TOEP_ERR_INVALID, "z pitch too small");
   cudaStream_t st = S(stream);
   const toep_taps* g = m->r->g;
+  if (m->mma && count >= 65535) m->mma = false;  // K-step tables hold uint16 source rows
+  if (m->mma && (s0 != m->mma_s0 || count != m->mma_count)) {
+    const int rc = mma_plan(m, s0, count, st);  // may fall back to the FFMA mix (tables too large)
+    if (rc != TOEP_OK) return rc;
+  }
   if (m->mma) {
-    if (s0 != m->mma_s0 || count != m->mma_count) {
-      const int rc = mma_plan(m, s0, count, st);
-      if (rc != TOEP_OK) return rc;
-    }
     MixMmaArgs a{};
     a.y = y;
     a.T = m->T;
@@ -980,6 +996,8 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.rows = m->d_mrows;
     a.g = m->d_mg;
     a.KS = m->KS;
+    a.nsrc4 = m->nsrc4;
+    a.ring = m->ring;
     a.N = m->N;
     a.KP = m->KP;
     a.K = g->length;

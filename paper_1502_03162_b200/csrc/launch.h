@@ -65,7 +65,7 @@ struct RenderMmaArgs {
   const float* f;        // [ears][lf_pad] resonance taps, zero padded
   int lf_pad;
   const void* g;         // [ears][nchunks][hi, lo][canonical chunk x kpad] fp16 (build_render_mma_tables)
-  const float* gscale;   // [ears][nchunks] chunk unscale 2^-q
+  const int* gexp;       // [ears][nchunks][128 + 1] G row exponents + "wide chunk" flag (build_render_mma_tables)
   int kpad;              // round_up(K, 16)
   int nchunks;           // ceil(dirs / render_mma_chunk())
   int dirs, ears;
@@ -80,11 +80,18 @@ bool render_mma_supported(int K, int lf_pad);
 int render_mma_kpad(int K);
 int render_mma_chunk();  // directions per G chunk (MMA N)
 size_t render_mma_gbytes(int ears, int dirs, int K);
+size_t render_mma_gexp_ints(int ears, int dirs);
 cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, int ears, int stride, int K,
-                                    void* g, float* gscale, cudaStream_t st);
+                                    void* g, int* gexp, cudaStream_t st);
 cudaError_t make_render_mma_map(float* out, int ears, int dirs, long long out_len, long long out_pitch,
                                 CUtensorMap* m);
-cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st);
+// side stream + fork/join events of one renderer (the concurrent fill launch)
+struct MmaFillStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, const MmaFillStreams& fs, int sm_count,
+                              cudaStream_t st);
 int render_mma_launches(int n_titems, int kpad, int lf_pad, int sm_count);
 
 // FFT (fft.cu): radix-2, power-of-two n; complex buffers interleaved.
@@ -183,19 +190,20 @@ cudaError_t launch_ear_pair_taps(const int2* rows, int dirs, int ears, int strid
 // tcgen05 (M = 128 time rows, K = 16 direction rows per step, N = ears x KP),
 // then z_e[t] = sum_o W[t-o][(e,o)].  The host plans K-steps of up to 16 rows
 // (a row = up to kMixRowSrcs sources of one direction, <= kMixKsSrcs per step).
-constexpr int kMixTile = 256;     // samples per tile (two 128-row blocks)
-constexpr int kMixRing = 160;     // 1 KB source slices in the shared-memory ring
+constexpr int kMixTile = 256;     // samples per tile (two 128-row blocks of the MMA)
 constexpr int kMixRowSrcs = 4;    // sources per direction row
 constexpr int kMixKsSrcs = 64;    // sources per K-step
 struct MixMmaArgs {
   const float* y;        // sources, row i at y + i * y_pitch (16-byte aligned rows), length T
   long long T;
   long long y_pitch;
-  const int* src;        // source rows in K-step order, each K-step padded to a multiple of 4 (tensor-map rows)
+  const unsigned short* src;  // source rows in K-step order, each K-step padded to a multiple of 4 (tensor-map rows)
   const int2* ks;        // [KS] {first entry in src (multiple of 4), padded count}
   const int* rows;       // [KS][16] row r: offset | count << 6 | (gamma_d + 128) << 9
   const unsigned char* g;  // [KS][hi, lo][canonical N x 16] fp16 of g * 2^gamma_d
   int KS;
+  int nsrc4;             // entries of src (all K-steps, padded)
+  int ring;              // 512-byte source slots in shared memory (mix_mma_ring)
   int N;                 // MMA N (multiple of 16, <= 208)
   int KP;                // columns per ear (K rounded up to 8)
   int K;                 // reflection length
@@ -217,7 +225,8 @@ struct MixMmaArgs {
 cudaError_t launch_mix_mma(const MixMmaArgs& a, const CUtensorMap& tm, int* bad_list, int* bad_count, int sm_count,
                            cudaStream_t st);
 cudaError_t make_mix_source_map(const float* y, long long T, long long rows, long long pitch, CUtensorMap* m);
-size_t mix_mma_smem(int N, int ears, int K);
+// shared-memory source-ring slots left next to the K-step tables; 0 = the tables do not fit
+int mix_mma_ring(int N, int ears, int K, int nsrc4, int KS);
 
 // z[e][t] = sum_g part[g][e][t]  (fixed order, fp32)
 cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long part_pitch, long long zlen,

@@ -32,23 +32,27 @@
 // those tiles with their own scale.  Results are a deterministic function of
 // the input.
 //
-// Persistent CTA per SM (20 warps), tile = 256 samples = two 128-row blocks:
-//   warp 0      source producer: one 1 KB cp.async.bulk per (source, tile)
-//               into a ring of 1 KB slots (measured 7.06 TB/s for this
-//               pattern, tools/microbench/gather_rate.cu); a K-step's slices
-//               complete on one mbarrier
+// Persistent CTA per SM (28 warps), tile = 256 samples = two 128-row blocks:
+//   warps 0, 3  source producers (one thread each, alternate gathers): the
+//               K-step's source rows, 4 per cp.async.bulk.tensor tile::gather4
+//               (1 KB per row) into a ring of 1 KB slots; a K-step's rows
+//               complete on one mbarrier (one gather4 occupies the TMA unit
+//               ~90 cycles, so 4 KB per op keeps it ahead of HBM; the pattern
+//               sustains ~7 TB/s, tools/microbench/gather_rate.cu)
 //   warp 1      G producer: the K-step's G (hi, lo; canonical K-major
 //               SWIZZLE_NONE, 13 KB at N = 208) into a 3-stage ring
 //   warp 2      MMA issuer: per K-step 2 row blocks x 3 products of
 //               tcgen05.mma M=128 N=208 K=16 (A from TMEM, G from smem)
-//   warps 4-11  A builders (lane = time): per K-step sum each row's <= 4
-//               source slices (direction rows), scale, split hi/lo, tcgen05.st
-//               into a 3-slot TMEM ring
-//   warps 12-19 epilogue: tcgen05.ld of W, overlap-add through warp
-//               shuffles into per-lane registers, combine of the 8 warps'
-//               windows in shared memory, z stores + overhang
-// TMEM: accumulators [0, 2N), A slots [416, 512) (32 columns each: row block
-// 0 hi/lo, row block 1 hi/lo).
+//   warps 4-19  A builders (lane = time; 4 warps per lane quarter: row block x
+//               half of the K-step's rows): sum each direction row's <= 4
+//               source slices, scale, split hi/lo, tcgen05.st into a 3-slot
+//               TMEM ring
+//   warps 20-27 epilogue (row block x lane quarter): tcgen05.ld of W,
+//               overlap-add through warp shuffles into per-lane registers,
+//               combine of the 8 windows in shared memory, z stores + overhang
+// The K-step tables (source rows, row info) are identical for every tile and
+// sit in shared memory; the source ring takes the rest.
+// TMEM: accumulators [0, 2N), A slots [416, 512) (32 columns each).
 #include <algorithm>
 #include <cstdio>
 #include <cuda_fp16.h>
@@ -59,13 +63,13 @@
 namespace toep {
 
 constexpr int kMxBuildWarps = 16;  // 4 per TMEM lane quarter: (row block, half of the K-step's 16 rows)
-constexpr int kMxEpiWarps = 4;     // one per lane quarter, both row blocks
+constexpr int kMxEpiWarps = 8;     // one per (row block, lane quarter)
 constexpr int kMxWarps = 4 + kMxBuildWarps + kMxEpiWarps;
 constexpr int kMxThreads = 32 * kMxWarps;
 constexpr int kMxKR = 16;      // K-step barrier ring
 constexpr int kMxGR = 3;       // G stages
-constexpr int kMxAR = 3;       // A slots in TMEM
-constexpr int kMxACol = 416;   // first A-slot column
+constexpr int kMxAR = 3;       // A slots in TMEM (32 columns each: row block 0 hi, lo, row block 1 hi, lo)
+constexpr int kMxACol = 416;   // first A-slot column (accumulators: 2 row blocks x N <= 416)
 constexpr int kMxSlotBytes = kMixTile * 4;
 constexpr int kMxWindows = 8;  // overlap-add windows per tile: (row block, lane quarter)
 
@@ -106,20 +110,33 @@ __device__ __forceinline__ float p2f(int e) { return __int_as_float((127 + e) <<
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct MxSmem {
-  int ring, g, ebuf, misc, bars, total;
+  int ring, g, ebuf, src, rows, ksn, misc, bars, total;
 };
-__host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr) {
+// Shared-memory layout; the source ring takes what the tables leave of the
+// 227 KB (ring = 0 asks for the ring size that fits, >= kMxMinRing slots).
+constexpr int kMxSmemMax = 227 * 1024 - 1024;  // static shared memory + slack
+constexpr int kMxMinRing = 2 * kMixKsSrcs;      // 1 KB slots (two full K-steps)
+__host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, int KS, int ring) {
   MxSmem L{};
-  L.ring = 0;
-  int off = kMixRing * kMxSlotBytes;
+  int off = 0;
   L.g = off;  // [kMxGR][hi, lo][N x 16] fp16
   off += kMxGR * N * 64;
-  L.ebuf = off;  // [2][kMxWindows][ears][32 * nr] fp32
-  off += 2 * kMxWindows * ears * 32 * nr * 4;
+  L.ebuf = off;  // [kMxWindows][ears][32 * nr] fp32
+  off += kMxWindows * ears * 32 * nr * 4;
+  L.src = off;  // [nsrc4] source rows of the K-steps (uint16, 8-byte aligned groups of 4)
+  off += ((nsrc4 + 7) & ~7) * 2;
+  L.rows = off;  // [KS][16] row info
+  off += KS * 64;
+  L.ksn = off;  // [KS] int2 {src offset, count}
+  off += ((KS + 1) & ~1) * 8;
   L.misc = off;  // builder max per warp [16]
   off += 64;
   L.bars = off;
   off += (2 * kMxKR + 2 * kMxGR + 2 * kMxAR + 2) * 8;
+  off = (off + 127) & ~127;
+  L.ring = off;
+  if (ring <= 0) ring = (kMxSmemMax - off) / kMxSlotBytes;
+  off += ring * kMxSlotBytes;
   L.total = off;
   return L;
 }
@@ -156,18 +173,27 @@ __device__ __forceinline__ int mx_tile_sexp(const MixMmaArgs& a, int j) {
 #else
 #define PROF_WAIT(slot, ...) __VA_ARGS__
 #endif
+#if !TOEP_MIX_PROF
+#define PROF_MARK(slot) \
+  do {                  \
+  } while (0)
+#endif
 
 template <int CH, int NR>
 __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw;
   const int N = a.N;
-  const MxSmem L = mx_smem(N, a.ears, NR);
+  const MxSmem L = mx_smem(N, a.ears, NR, a.nsrc4, a.KS, a.ring);
+  const int RING = a.ring;
   const int gbytes = N * 64;
   float* ring = reinterpret_cast<float*>(sm + L.ring);
   unsigned char* sG = sm + L.g;
   float* ebuf = reinterpret_cast<float*>(sm + L.ebuf);
   float* s_bmax = reinterpret_cast<float*>(sm + L.misc);
+  uint2* s_src4 = reinterpret_cast<uint2*>(sm + L.src);  // 4 x uint16 per gather
+  int4* s_rows4 = reinterpret_cast<int4*>(sm + L.rows);
+  int2* s_ksn = reinterpret_cast<int2*>(sm + L.ksn);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
   uint64_t* src_full = bars;
   uint64_t* src_empty = src_full + kMxKR;
@@ -180,7 +206,14 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   __shared__ unsigned s_tbase;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #if TOEP_MIX_PROF
-  long long prof[4] = {0, 0, 0, 0};
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long _tp = 0;
+#define PROF_MARK(slot)                      \
+  do {                                       \
+    const long long _n = clock64();          \
+    prof[slot] += _n - _tp;                  \
+    _tp = _n;                                \
+  } while (0)
   const long long t_start = clock64();
 #endif
 
@@ -202,6 +235,10 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
     mbar_init(acc_empty, kMxEpiWarps);
     mbar_fence_init();
   }
+  // the K-step tables (identical for every tile) -> shared memory
+  for (int i = tid; i < (a.nsrc4 >> 2); i += kMxThreads) s_src4[i] = __ldg(reinterpret_cast<const uint2*>(a.src) + i);
+  for (int i = tid; i < a.KS * 4; i += kMxThreads) s_rows4[i] = __ldg(reinterpret_cast<const int4*>(a.rows) + i);
+  for (int i = tid; i < a.KS; i += kMxThreads) s_ksn[i] = __ldg(a.ks + i);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -214,40 +251,46 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   tiles.cnt = a.bad_list ? *a.bad_count : 0;
   const int KS = a.KS;
 
-  if (warp == 0) {
-    // ===== source producer: the K-step's source rows (padded to 4) as tile::gather4
-    //       tensor copies, lane g issuing gather g; next K-step's rows prefetched =====
-    long long seq = 0, fseq = 0;  // K-steps issued / released
-    int pos = 0;                  // next free slot (a K-step never wraps: its slots restart at 0)
-    int held = 0;                 // slots held by unreleased K-steps (incl. skipped tails)
-    int hold[kMxKR];              // slots each in-flight K-step holds
-    const int4* src4 = reinterpret_cast<const int4*>(a.src);
-    int2 info = __ldg(a.ks);
-    int4 nxt = lane < (info.y >> 2) ? __ldg(src4 + (info.x >> 2) + lane) : make_int4(0, 0, 0, 0);
-    for (int i = 0;; ++i) {
-      const int j = tiles.at(i);
-      if (j < 0) break;
-      const int col = j * kMixTile;
-      for (int ks = 0; ks < KS; ++ks) {
-        const int n = info.y;  // multiple of 4
-        const int4 cur = nxt;
-        info = __ldg(a.ks + (ks + 1 < KS ? ks + 1 : 0));
-        nxt = lane < (info.y >> 2) ? __ldg(src4 + (info.x >> 2) + lane) : make_int4(0, 0, 0, 0);
-        const int skip = pos + n > kMixRing ? kMixRing - pos : 0;
-        while (seq - fseq >= kMxKR || held + skip + n > kMixRing) {
-          PROF_WAIT(0, mbar_wait(&src_empty[fseq % kMxKR], (unsigned)((fseq / kMxKR) & 1)));
-          held -= hold[fseq % kMxKR];
-          ++fseq;
+  if (warp == 0 || warp == 3) {
+    // ===== source producers (one thread each in warps 0 and 3, on different SM
+    //       sub-partitions): the K-step's source rows, 4 per tile::gather4,
+    //       alternate gathers per thread (one gather4 costs ~100 issue cycles);
+    //       both track the ring identically, warp 0 posts the expected bytes =====
+    const int pid = warp == 0 ? 0 : 1;
+    if (elect_one()) {
+      long long seq = 0, fseq = 0;  // K-steps issued / released
+      int pos = 0;                  // next free slot (a K-step never wraps: its slots restart at 0)
+      int held = 0;                 // slots held by unreleased K-steps (incl. skipped tails)
+      int hold[kMxKR];              // slots each in-flight K-step holds
+      for (int i = 0;; ++i) {
+        const int j = tiles.at(i);
+        if (j < 0) break;
+        const int col = j * kMixTile;
+        for (int ks = 0; ks < KS; ++ks) {
+          const int2 info = s_ksn[ks];
+          const int n = info.y;  // multiple of 4
+          const int skip = pos + n > RING ? RING - pos : 0;
+          while (seq - fseq >= kMxKR || held + skip + n > RING) {
+            PROF_WAIT(0, mbar_wait(&src_empty[fseq % kMxKR], (unsigned)((fseq / kMxKR) & 1)));
+            held -= hold[fseq % kMxKR];
+            ++fseq;
+          }
+          if (pos + n > RING) pos = 0;
+          hold[seq % kMxKR] = skip + n;
+          held += skip + n;
+          uint64_t* bar = &src_full[seq % kMxKR];
+          if (pid == 0) mbar_arrive_expect_tx(bar, (unsigned)(n * kMxSlotBytes));
+          const uint2* sl = s_src4 + (info.x >> 2);
+          float* dst = ring + pos * kMixTile;
+#pragma unroll 4
+          for (int g = pid; g < (n >> 2); g += 2) {
+            const uint2 r2 = sl[g];
+            const int4 r = make_int4((int)(r2.x & 0xffffu), (int)(r2.x >> 16), (int)(r2.y & 0xffffu), (int)(r2.y >> 16));
+            mx_gather4(dst + 4 * g * kMixTile, &tm, col, r, bar);
+          }
+          pos += n;
+          ++seq;
         }
-        if (pos + n > kMixRing) pos = 0;
-        hold[seq % kMxKR] = skip + n;
-        held += skip + n;
-        uint64_t* bar = &src_full[seq % kMxKR];
-        if (lane == 0) mbar_arrive_expect_tx(bar, (unsigned)(n * kMxSlotBytes));
-        __syncwarp();
-        if (4 * lane < n) mx_gather4(ring + (pos + 4 * lane) * kMixTile, &tm, col, cur, bar);
-        pos += n;
-        ++seq;
       }
     }
   } else if (warp == 1) {
@@ -269,7 +312,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       }
     }
   } else if (warp == 2) {
-    // ===== MMA issuer =====
+    // ===== MMA issuer: per K-step 2 row blocks x 3 products =====
     if (elect_one()) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const unsigned sg = smem_u32(sG);
@@ -278,6 +321,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       for (int i = 0;; ++i) {
         if (tiles.at(i) < 0) break;
         PROF_WAIT(2, mbar_wait_sleep(acc_empty, cph ^ 1u));  // the epilogue has drained the accumulators
+        cph ^= 1u;
         tmem_fence_after();
         for (int ks = 0; ks < KS; ++ks) {
           PROF_WAIT(0, mbar_wait(&g_full[gs], gph));
@@ -304,7 +348,6 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           }
         }
         mx_commit(acc_full);
-        cph ^= 1u;
       }
     }
   } else if (warp >= 4 && warp < 4 + kMxBuildWarps) {
@@ -317,10 +360,9 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
     int pos = 0, as = 0;
     unsigned aph = 0;
     float chk0 = 0.f, chk1 = 0.f;
-    // row info of the next K-step is loaded one K-step ahead (8 rows x 4 B = 2 int4)
-    const int4* rtab = reinterpret_cast<const int4*>(a.rows) + 2 * half;
-    int4 nr0 = __ldg(rtab), nr1 = __ldg(rtab + 1);
-    int nn = __ldg(&a.ks[0].y);
+#if TOEP_MIX_PROF
+    _tp = clock64();
+#endif
     for (int i = 0;; ++i) {
       const int j = tiles.at(i);
       if (j < 0) break;
@@ -330,43 +372,38 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       const float S = p2f(sexp);
       float amax = 0.f;
       for (int ks = 0; ks < KS; ++ks) {
-        const int n = nn;
-        const int ri[8] = {nr0.x, nr0.y, nr0.z, nr0.w, nr1.x, nr1.y, nr1.z, nr1.w};
-        {
-          const int kn = ks + 1 < KS ? ks + 1 : 0;
-          nr0 = __ldg(rtab + 4 * kn);
-          nr1 = __ldg(rtab + 4 * kn + 1);
-          nn = __ldg(&a.ks[kn].y);
-        }
-        if (pos + n > kMixRing) pos = 0;
-        int off[8], cnt[8];
-        float mul[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          off[r] = ri[r] & 63;
-          cnt[r] = (ri[r] >> 6) & 7;
-          mul[r] = __int_as_float((255 - ((ri[r] >> 9) & 0xff)) << 23);  // 2^-gamma_d
-        }
+        const int n = s_ksn[ks].y;
+        const int4 ra = s_rows4[4 * ks + 2 * half], rbv = s_rows4[4 * ks + 2 * half + 1];  // this warp's 8 rows
+        const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
+        if (pos + n > RING) pos = 0;
+        PROF_MARK(3);
         PROF_WAIT(0, mbar_wait(&src_full[seq % kMxKR], (unsigned)((seq / kMxKR) & 1)));
+        PROF_MARK(7);
         const float* base = ring + pos * kMixTile + tt;
         float v[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const float* p = base + off[r] * kMixTile;
-          float s0 = 0.f, s1 = 0.f;
-          if (cnt[r] > 0) s0 = p[0];
-          if (cnt[r] > 1) s1 = p[kMixTile];
-          if (cnt[r] > 2) s0 += p[2 * kMixTile];
-          if (cnt[r] > 3) s1 += p[3 * kMixTile];
-          v[r] = s0 + s1;
+        for (int h4 = 0; h4 < 2; ++h4) {  // 16 predicated loads in flight, then the adds
+          float L0[16];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int rr = 4 * h4 + r;
+            const int cnt = (ri[rr] >> 6) & 7;
+            const float* p = base + (ri[rr] & 63) * kMixTile;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) L0[4 * r + k] = cnt > k ? p[k * kMixTile] : 0.f;
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r) v[4 * h4 + r] = (L0[4 * r] + L0[4 * r + 2]) + (L0[4 * r + 1] + L0[4 * r + 3]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&src_empty[seq % kMxKR]);
+        PROF_MARK(4);
         unsigned hw[4], lw[4];
 #pragma unroll
         for (int r = 0; r < 8; r += 2) {
-          float x0 = valid ? v[r] * mul[r] : 0.f;  // Y_d 2^-gamma_d
-          float x1 = valid ? v[r + 1] * mul[r + 1] : 0.f;
+          // Y_d 2^-gamma_d  (row multiplier 2^-gamma_d from the row's exponent field)
+          float x0 = valid ? v[r] * __int_as_float((255 - ((ri[r] >> 9) & 0xff)) << 23) : 0.f;
+          float x1 = valid ? v[r + 1] * __int_as_float((255 - ((ri[r + 1] >> 9) & 0xff)) << 23) : 0.f;
           chk0 = fmaf(x0, 0.f, chk0);
           chk1 = fmaf(x1, 0.f, chk1);
           amax = fmaxf(amax, fmaxf(fabsf(x0), fabsf(x1)));
@@ -377,7 +414,9 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           hw[r / 2] = h;
           lw[r / 2] = mx_h2(x0 - hf.x, x1 - hf.y);
         }
+        PROF_MARK(5);
         PROF_WAIT(1, mbar_wait(&a_empty[as], aph ^ 1u));
+        PROF_MARK(7);
         tmem_fence_after();
         const unsigned ta = ta0 + (unsigned)(32 * as);
         mx_st4(ta, hw[0], hw[1], hw[2], hw[3]);
@@ -386,6 +425,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         tmem_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[as]);
+        PROF_MARK(6);
         if (++as == kMxAR) {
           as = 0;
           aph ^= 1u;
@@ -408,64 +448,61 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
     }
     if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk0 + chk1)) && lane == 0) atomicOr(a.nonfinite, 1);
   } else if (warp >= 4 + kMxBuildWarps) {
-    // ===== epilogue: W -> overlap-add -> z (one warp per lane quarter, both row blocks) =====
-    const int q = warp & 3;
+    // ===== epilogue: W -> overlap-add -> z (one warp per row block x lane quarter) =====
+    const int ew = warp - 4 - kMxBuildWarps;
+    const int q = warp & 3, rb = ew >> 2;
+    const unsigned tq = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(rb * N);
     const int ears = a.ears, K = a.K, KP = a.KP;
     const int win = 32 * NR;
     unsigned cph = 0;
     for (int i = 0;; ++i) {
       const int j = tiles.at(i);
       if (j < 0) break;
-      float* eb = ebuf + ((i & 1) * kMxWindows * ears) * win;
+      float* eb = ebuf;
+      float R0[NR], R1[NR];
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        R0[k] = 0.f;
+        R1[k] = 0.f;
+      }
       PROF_WAIT(0, mbar_wait(acc_full, cph));
       cph ^= 1u;
       tmem_fence_after();
-#pragma unroll 1
-      for (int rb = 0; rb < 2; ++rb) {
-        const unsigned tq = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(rb * N);
-        float R0[NR], R1[NR];
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-          R0[k] = 0.f;
-          R1[k] = 0.f;
+      for (int c = 0; c < CH; ++c) {
+        float w0[16], w1[16];
+        tmem_ld16(w0, tq + (unsigned)(16 * c));
+        if (ears > 1) tmem_ld16(w1, tq + (unsigned)(KP + 16 * c));
+        tmem_wait_ld();
+        if (c == CH - 1) {  // every accumulator column this warp reads has been read
+          tmem_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty);
         }
+        // W[t][o] (lane t) belongs to window position t + o: lane L collects
+        // the positions = L (mod 32) from lane (L - o) mod 32
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          float w0[16], w1[16];
-          tmem_ld16(w0, tq + (unsigned)(16 * c));
-          if (ears > 1) tmem_ld16(w1, tq + (unsigned)(KP + 16 * c));
-          tmem_wait_ld();
-          if (rb == 1 && c == CH - 1) {  // every accumulator column this warp reads has been read
-            tmem_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty);
-          }
-          // W[t][o] (lane t) belongs to window position t + o: lane L collects
-          // the positions = L (mod 32) from lane (L - o) mod 32
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const int o = 16 * c + jj;
-            if (o < K) {
-              const int srcl = (lane - o) & 31;
-              const float x0 = __shfl_sync(0xffffffffu, w0[jj], srcl);
-              const float x1 = ears > 1 ? __shfl_sync(0xffffffffu, w1[jj], srcl) : 0.f;
-              const int kb = o >> 5;
-              if (srcl + (o & 31) < 32) {
-                R0[kb] += x0;
-                R1[kb] += x1;
-              } else if (kb + 1 < NR) {
-                R0[kb + 1] += x0;
-                R1[kb + 1] += x1;
-              }
+        for (int jj = 0; jj < 16; ++jj) {
+          const int o = 16 * c + jj;
+          if (o < K) {
+            const int srcl = (lane - o) & 31;
+            const float x0 = __shfl_sync(0xffffffffu, w0[jj], srcl);
+            const float x1 = ears > 1 ? __shfl_sync(0xffffffffu, w1[jj], srcl) : 0.f;
+            const int kb = o >> 5;
+            if (srcl + (o & 31) < 32) {
+              R0[kb] += x0;
+              R1[kb] += x1;
+            } else if (kb + 1 < NR) {
+              R0[kb + 1] += x0;
+              R1[kb + 1] += x1;
             }
           }
         }
-        const int w = 4 * rb + q;
+      }
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-          eb[(w * ears) * win + 32 * k + lane] = R0[k];
-          if (ears > 1) eb[(w * ears + 1) * win + 32 * k + lane] = R1[k];
-        }
+      for (int k = 0; k < NR; ++k) {
+        eb[(ew * ears) * win + 32 * k + lane] = R0[k];
+        if (ears > 1) eb[(ew * ears + 1) * win + 32 * k + lane] = R1[k];
       }
       named_sync(2, 32 * kMxEpiWarps);
       // combine the 8 windows (fixed order): position P of the tile's 256 + K - 1
@@ -488,13 +525,14 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           a.ovh[((long long)j * ears + e) * a.ovh_pitch + (P - kMixTile)] = acc;
         }
       }
+      named_sync(2, 32 * kMxEpiWarps);  // the windows are rewritten for the next tile
     }
   }
 #if TOEP_MIX_PROF
-  if (blockIdx.x == 0 && (warp <= 2 || warp == 4 || warp == 4 + kMxBuildWarps) &&
+  if (blockIdx.x == 0 && (warp <= 3 || warp == 4 || warp == 4 + kMxBuildWarps) &&
       (lane == 0 || prof[0] + prof[1] + prof[2] > 0) && (warp != 0 || lane == 0))
-    printf("mixprof warp %d total %lld waits: %lld %lld %lld\n", warp, clock64() - t_start, prof[0], prof[1],
-           prof[2]);
+    printf("mixprof warp %d total %lld waits: %lld %lld %lld phases: top %lld loads %lld conv %lld st %lld\n", warp,
+           clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5], prof[6]);
 #endif
   tmem_fence_before();
   __syncthreads();
@@ -550,14 +588,16 @@ __global__ void k_mix_carry(float* __restrict__ z, long long z_pitch, long long 
 
 int mix_mma_nr(int K) { return (32 + K - 1 + 31) / 32; }
 
-size_t mix_mma_smem(int N, int ears, int K) {
+// ring slots left by the tables (0 if the tables do not leave kMxMinRing slots)
+int mix_mma_ring(int N, int ears, int K, int nsrc4, int KS) {
   const int nr = mix_mma_nr(K) <= 5 ? 5 : 8;
-  return (size_t)mx_smem(N, ears, nr).total;
+  const int ring = (kMxSmemMax - mx_smem(N, ears, nr, nsrc4, KS, 1).ring) / kMxSlotBytes;
+  return ring >= kMxMinRing ? ring : 0;
 }
 
 template <int CH, int NR>
 static cudaError_t launch_mix_mma_t(const MixMmaArgs& a, const CUtensorMap& tm, int grid, cudaStream_t st) {
-  const int bytes = mx_smem(a.N, a.ears, NR).total;
+  const int bytes = mx_smem(a.N, a.ears, NR, a.nsrc4, a.KS, a.ring).total;
   auto kern = k_mix_mma<CH, NR>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), bytes);
   if (e != cudaSuccess) return e;

@@ -49,6 +49,7 @@
 //                 [32 directions][32 t] blocks in shared memory, TMA tensor
 //                 stores (3-D map {t, direction, ear} clips padding directions)
 #include <algorithm>
+#include <climits>
 #include <mutex>
 #include <cstdio>
 #include <cuda_fp16.h>
@@ -74,6 +75,9 @@ namespace toep {
 #else
 #define PW(slot, ...) __VA_ARGS__
 #endif
+// 2^e for e in [-126, 127] (exact; callers split larger exponents in two);
+// clamped at the ends, where the product they scale under/overflows anyway
+__device__ __forceinline__ float exp2i(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
 constexpr int kMmaM = 128;        // outputs per t-tile
 constexpr int kMmaN = 128;        // directions per chunk (M = 128, N = 128: full tensor rate, N = 64 runs at half)
 constexpr int kMmaBuilderWarps = 8;  // two per TMEM lane quarter
@@ -174,7 +178,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const float*
 }
 
 struct MmaSmem {
-  int b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, bars_off, total, nstg;
+  int b_off, st_off, y_off, yf_off, f_off, red_off, sc_off, fac_off, bars_off, total, nstg;
 };
 
 __host__ __device__ inline MmaSmem mma_smem_n(int kpad, int lf_pad, int nstg) {
@@ -193,6 +197,8 @@ __host__ __device__ inline MmaSmem mma_smem_n(int kpad, int lf_pad, int nstg) {
   off += 32 * 4;
   L.sc_off = off;
   off += 8 * 4;
+  L.fac_off = off;  // wide G chunks: per-column unscale factors [epilogue warps][2][64]
+  off += kMmaEpiWarps * 2 * 64 * 4;
   L.bars_off = off;
   off += (12 + 2 * kMmaBStages + 5) * 8;
   L.total = off + 1024;  // alignment slack
@@ -413,11 +419,13 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       builders_sync();
       mx = 0.f;
       for (int w = 0; w < kMmaBuilderWarps; ++w) mx = fmaxf(mx, s_red[w]);
-      const int sexp = mx > 0.f ? 13 - ilogbf(mx) : 0;  // max |yf| * 2^sexp in [2^13, 2^14)
-      const float scale = ldexpf(1.f, sexp);
+      // max |yf| * 2^sexp in [2^13, 2^14); sexp in [-114, 162] (subnormal tiles
+      // included), applied as two exact power-of-two factors so neither overflows
+      const int sexp = mx > 0.f ? 13 - ilogbf(mx) : 0;
+      const float sc1 = exp2i(sexp / 2), sc2 = exp2i(sexp - sexp / 2);
       if (bt == 0) {
         PW(5, mbar_wait_sleep(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1)));
-        s_sc[nitem & 1] = ldexpf(1.f, -sexp);
+        s_sc[nitem & 1] = __int_as_float(sexp);
         mbar_arrive(&sc_full[nitem & 1]);
       }
       if (ring) {
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             unsigned w[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float x0 = src[-2 * (j0 + j)] * scale, x1 = src[-2 * (j0 + j) - 1] * scale;
+              const float x0 = src[-2 * (j0 + j)] * sc1 * sc2, x1 = src[-2 * (j0 + j) - 1] * sc1 * sc2;
               const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
               w[j] = part == 0 ? pack_half2(h0, h1)
                                : pack_half2(__float2half_rn(x0 - __half2float(h0)),
@@ -467,7 +475,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
           unsigned hw[8], lw[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float x0 = src[-2 * (j0 + j)] * scale, x1 = src[-2 * (j0 + j) - 1] * scale;
+            const float x0 = src[-2 * (j0 + j)] * sc1 * sc2, x1 = src[-2 * (j0 + j) - 1] * sc1 * sc2;
             const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
             hw[j] = pack_half2(h0, h1);
             lw[j] = pack_half2(__float2half_rn(x0 - __half2float(h0)), __float2half_rn(x1 - __half2float(h1)));
@@ -496,7 +504,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     unsigned aph = 0;
     long long cur = -1;
     int nitem = -1;
-    float unscale = 1.f;
+    int tsexp = 0;
+    float* fa = reinterpret_cast<float*>(sm + L.fac_off) + ew * 128;  // [2][64] factors of this warp's columns
     for (long long u = u0; u < u1; ++u) {
       const long long item = u / nch;
       const int c = (int)(u % nch);
@@ -508,13 +517,32 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         }
         ++nitem;
         mbar_wait_sleep(&sc_full[nitem & 1], (unsigned)((nitem >> 1) & 1));
-        unscale = s_sc[nitem & 1];
+        tsexp = __float_as_int(s_sc[nitem & 1]);
         cur = item;
       }
       PW(6, mbar_wait_sleep(&acc_full[as], aph));
       tmem_fence_after();
       const long long t0 = (long long)ti * kMmaM + 32 * q;
-      const float unscale_c = unscale * __ldg(a.gscale + (long long)e * nch + c);  // tile 2^-s x chunk 2^-q
+      // unscale = 2^-(tile exponent + G exponent): one factor per chunk, or per
+      // column (direction) when the chunk's directions span more than 2^12 in
+      // gain ("wide"); two factors whenever one would leave the normal range
+      const int* gx = a.gexp + ((long long)e * nch + c) * (kMmaN + 1);
+      const bool wide = gx[kMmaN] != 0;
+      float uc1 = 1.f, uc2 = 1.f;
+      if (!wide) {
+        const int E = tsexp + gx[0];
+        uc1 = exp2i(-(E / 2));
+        uc2 = exp2i(-(E - E / 2));
+      } else {
+        __syncwarp();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int E = tsexp + gx[64 * half + 32 * h2 + lane];
+          fa[32 * h2 + lane] = exp2i(-(E / 2));
+          fa[64 + 32 * h2 + lane] = exp2i(-(E - E / 2));
+        }
+        __syncwarp();
+      }
       if (t0 < a.out_len && ti < a.t_end) {
 #pragma unroll 1
         for (int blk = 0; blk < 2; ++blk) {
@@ -532,8 +560,14 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             float v[16];
             tmem_ld16(v, tq + (unsigned)(as * kMmaN + col + cb));
             tmem_wait_ld();
+            if (!wide) {
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * unscale_c;
+              for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * uc1 * uc2;
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj)
+                stg[(cb + jj) * 32 + lane] = v[jj] * fa[32 * blk + cb + jj] * fa[64 + 32 * blk + cb + jj];
+            }
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -565,13 +599,16 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
 }
 
 // G[e][c] chunk = [hi, lo][canonical 128 x kpad] fp16 of the dense rows of
-// directions 128c .. 128c+127, scaled by 2^q with max |g| over the chunk * 2^q
-// in [2^13, 2^14); gscale[e][c] = 2^-q.  One block of kMmaN threads (one per
-// direction row) per (ear, chunk).
+// directions 128c .. 128c+127.  Rows are scaled by powers of two so that the
+// largest |g| lands in [2^13, 2^14): one exponent for the whole chunk when its
+// directions' maxima lie within 2^12 of each other (every row keeps the full
+// hi/lo precision), else one per row ("wide" chunk; the epilogue unscales per
+// column).  gexp[e][c] = {128 row exponents, wide flag}.  One block of kMmaN
+// threads (one per direction row) per (ear, chunk).
 __global__ void __launch_bounds__(kMmaN) k_build_gmma(const int2* __restrict__ raw, const int* __restrict__ nnz,
                                                      int dirs, int stride, int kpad, int nchunks,
-                                                     __half* __restrict__ g, float* __restrict__ gscale) {
-  __shared__ float s_mx[kMmaN / 32];
+                                                     __half* __restrict__ g, int* __restrict__ gexp) {
+  __shared__ int s_lo[kMmaN / 32], s_hi[kMmaN / 32];
   const int c = blockIdx.x, e = blockIdx.y, r = threadIdx.x, d = c * kMmaN + r;
   const bool real = d < dirs;
   const int row = e * dirs + d;
@@ -579,14 +616,31 @@ __global__ void __launch_bounds__(kMmaN) k_build_gmma(const int2* __restrict__ r
   const int2* taps = raw + (long long)row * stride;
   float mx = 0.f;
   for (int k = 0; k < n; ++k) mx = fmaxf(mx, fabsf(__int_as_float(taps[k].y)));
+  // row exponent: 13 - ilogb(max); rows without taps do not constrain the chunk
+  const int q = mx > 0.f ? 13 - ilogbf(mx) : 0;
+  int lo = mx > 0.f ? q : INT_MAX, hi = mx > 0.f ? q : INT_MIN;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((r & 31) == 0) s_mx[r >> 5] = mx;
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((r & 31) == 0) {
+    s_lo[r >> 5] = lo;
+    s_hi[r >> 5] = hi;
+  }
   __syncthreads();
-  mx = 0.f;
-  for (int w = 0; w < kMmaN / 32; ++w) mx = fmaxf(mx, s_mx[w]);
-  const int qexp = mx > 0.f ? 13 - ilogbf(mx) : 0;
-  if (r == 0) gscale[(long long)e * nchunks + c] = ldexpf(1.f, -qexp);
+  lo = INT_MAX;
+  hi = INT_MIN;
+  for (int w = 0; w < kMmaN / 32; ++w) {
+    lo = min(lo, s_lo[w]);
+    hi = max(hi, s_hi[w]);
+  }
+  const bool wide = hi != INT_MIN && hi - lo > 12;
+  const int qc = lo == INT_MAX ? 0 : lo;  // the loudest row's exponent
+  const int qexp = wide ? (mx > 0.f ? q : qc) : qc;
+  int* gx = gexp + ((long long)e * nchunks + c) * (kMmaN + 1);
+  gx[r] = qexp;
+  if (r == 0) gx[kMmaN] = wide ? 1 : 0;
   unsigned char* base = reinterpret_cast<unsigned char*>(g) + ((long long)e * nchunks + c) * 2 * kMmaN * kpad * 2;
   for (int k = 0; k < n; ++k) {  // taps are unique offsets; everything else stays zero (memset)
     const int o = taps[k].x;
@@ -614,14 +668,18 @@ size_t render_mma_gbytes(int ears, int dirs, int K) {
   return (size_t)ears * nch * 2 * kMmaN * kp * 2;
 }
 
+size_t render_mma_gexp_ints(int ears, int dirs) {
+  return (size_t)ears * ((dirs + kMmaN - 1) / kMmaN) * (kMmaN + 1);
+}
+
 cudaError_t build_render_mma_tables(const int2* raw, const int* nnz, int dirs, int ears, int stride, int K,
-                                    void* g, float* gscale, cudaStream_t st) {
+                                    void* g, int* gexp, cudaStream_t st) {
   const int kp = render_mma_kpad(K);
   const int nch = (dirs + kMmaN - 1) / kMmaN;
   cudaError_t e = cudaMemsetAsync(g, 0, render_mma_gbytes(ears, dirs, K), st);
   if (e != cudaSuccess) return e;
   k_build_gmma<<<dim3(nch, ears), kMmaN, 0, st>>>(raw, nnz, dirs, stride, kp, nch, reinterpret_cast<__half*>(g),
-                                                 gscale);
+                                                 gexp);
   return cudaGetLastError();
 }
 
@@ -690,47 +748,47 @@ int render_mma_launches(int n_titems, int kpad, int lf_pad, int sm_count) {
 // B200's 148 SMs), plus, concurrently on a side stream, small clusters on the
 // SMs left over; each launch takes a share of every ear's tiles in proportion
 // to its measured throughput.
-cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, int sm_count, cudaStream_t st) {
+cudaError_t launch_render_mma(const RenderMmaArgs& a, const CUtensorMap& map, const MmaFillStreams& fs,
+                              int sm_count, cudaStream_t st) {
   const MmaSmem L = mma_smem(a.kpad, a.lf_pad);
-  struct Fill {  // per device: the cluster count and the side stream/events of the fill launch
-    int clusters = 0;
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-  };
   static std::mutex mu;
-  static Fill fills[64];
+  static int clusters[64] = {};  // per device: co-resident kMmaCluster-CTA clusters
   int dev = 0;
   cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  std::lock_guard<std::mutex> lk(mu);  // fork -> launches -> join is one unit per call
-  Fill& F = fills[dev];
-  if (!F.clusters) {
-    if ((err = cudaStreamCreateWithFlags(&F.side, cudaStreamNonBlocking)) != cudaSuccess) return err;
-    if ((err = cudaEventCreateWithFlags(&F.fork, cudaEventDisableTiming)) != cudaSuccess) return err;
-    if ((err = cudaEventCreateWithFlags(&F.join, cudaEventDisableTiming)) != cudaSuccess) return err;
-    F.clusters = max_clusters_for<kMmaCluster>(sm_count, L.total);
-    if (getenv("TOEP_VERBOSE"))
-      fprintf(stderr, "k_render_mma: %d clusters of %d CTAs + fill on %d SMs\n", F.clusters, kMmaCluster, sm_count);
+  int ncl;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!clusters[dev]) {
+      clusters[dev] = max_clusters_for<kMmaCluster>(sm_count, L.total);
+      if (getenv("TOEP_VERBOSE"))
+        fprintf(stderr, "k_render_mma: %d clusters of %d CTAs + fill on %d SMs\n", clusters[dev], kMmaCluster,
+                sm_count);
+    }
+    ncl = clusters[dev];
   }
-  const int main_ctas = F.clusters * kMmaCluster;
+  const int main_ctas = ncl * kMmaCluster;
   const int fill = TOEP_MMA_FILL ? (sm_count - main_ctas) / kMmaFillCluster * kMmaFillCluster : 0;
   RenderMmaArgs m = a;
   m.t_begin = 0;
   m.t_end = a.n_titems;
-  if (fill <= 0 || a.n_titems < 4 * sm_count) return launch_mma_cl<kMmaCluster>(m, map, main_ctas, L.total, st);
+  // the fill launch runs on the renderer's own side stream (fork/join events),
+  // so distinct renderers never share a stream; without one, one launch
+  if (fill <= 0 || a.n_titems < 4 * sm_count || !fs.side)
+    return launch_mma_cl<kMmaCluster>(m, map, main_ctas, L.total, st);
   const double share = main_ctas / (main_ctas + TOEP_MMA_FILL_RATE * fill);
   const int split = std::min(a.n_titems, ((int)(a.n_titems * share) + kMmaCluster - 1) / kMmaCluster * kMmaCluster);
   m.t_end = split;
   RenderMmaArgs f = a;
   f.t_begin = split;
   f.t_end = a.n_titems;
-  if ((err = cudaEventRecord(F.fork, st)) != cudaSuccess) return err;
-  if ((err = cudaStreamWaitEvent(F.side, F.fork, 0)) != cudaSuccess) return err;
+  if ((err = cudaEventRecord(fs.fork, st)) != cudaSuccess) return err;
+  if ((err = cudaStreamWaitEvent(fs.side, fs.fork, 0)) != cudaSuccess) return err;
   if ((err = launch_mma_cl<kMmaCluster>(m, map, main_ctas, L.total, st)) != cudaSuccess) return err;
-  if ((err = launch_mma_cl<kMmaFillCluster>(f, map, fill, L.total, F.side)) != cudaSuccess) return err;
-  if ((err = cudaEventRecord(F.join, F.side)) != cudaSuccess) return err;
-  return cudaStreamWaitEvent(st, F.join, 0);
+  if ((err = launch_mma_cl<kMmaFillCluster>(f, map, fill, L.total, fs.side)) != cudaSuccess) return err;
+  if ((err = cudaEventRecord(fs.join, fs.side)) != cudaSuccess) return err;
+  return cudaStreamWaitEvent(st, fs.join, 0);
 }
 
 }  // namespace toep

@@ -730,6 +730,7 @@ struct toep_mixer {
   unsigned short* d_msrc = nullptr;
   int2* d_mks = nullptr;
   int* d_mrows = nullptr;
+  float* d_mrowf = nullptr;
   unsigned char* d_mg = nullptr;
   float* d_ovh = nullptr;
   float* d_tmax = nullptr;
@@ -748,12 +749,14 @@ static bool mix_mma_enabled() {
 }
 
 static void mma_plan_free(toep_mixer* m) {
-  for (void* p : {(void*)m->d_msrc, (void*)m->d_mks, (void*)m->d_mrows, (void*)m->d_mg, (void*)m->d_ovh,
+  for (void* p : {(void*)m->d_msrc, (void*)m->d_mks, (void*)m->d_mrows, (void*)m->d_mrowf, (void*)m->d_mg,
+                  (void*)m->d_ovh,
                   (void*)m->d_tmax, (void*)m->d_bad})
     if (p) cudaFree(p);
   m->d_msrc = nullptr;
   m->d_mks = nullptr;
   m->d_mrows = nullptr;
+  m->d_mrowf = nullptr;
   m->d_mg = nullptr;
   m->d_ovh = nullptr;
   m->d_tmax = nullptr;
@@ -794,6 +797,8 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   }
   std::vector<int2> ks;
   std::vector<int> rinfo;    // [KS][16] offset | count << 6 | (gamma_d + 128) << 9
+  std::vector<float> rowf;   // [KS][16] main-pass multipliers 2^(sexp - gamma_d)
+  bool clamped = false;
   std::vector<int> ks_dirs;  // [KS][16] direction per row (-1 empty), gamma_d
   std::vector<unsigned short> src;  // K-step source lists, each padded to a multiple of 4 with an out-of-range row
   for (size_t i = 0; i < rows.size();) {
@@ -818,10 +823,14 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
         int gam = mx > 0.f ? 13 - std::ilogb(mx) : 0;
         gam = std::max(-126, std::min(126, gam));
         rinfo.push_back((w.first - start) | (w.cnt << 6) | ((gam + 128) << 9));
+        const int em = m->sexp - gam;
+        clamped |= em < -126 || em > 127;
+        rowf.push_back(std::ldexp(1.f, std::max(-126, std::min(127, em))));
         ks_dirs.push_back(w.d);
         ks_dirs.push_back(gam);
       } else {
-        rinfo.push_back(128 << 9);  // empty row (multiplier 2^0)
+        rinfo.push_back(128 << 9);  // empty row
+        rowf.push_back(0.f);
         ks_dirs.push_back(-1);
         ks_dirs.push_back(0);
       }
@@ -854,6 +863,10 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
       }
     }
   }
+  if (clamped) {  // a direction's gain is so far from the others that 2^(sexp - gamma) leaves fp32
+    m->mma = false;
+    return TOEP_OK;
+  }
   m->KS = KS;
   m->nsrc4 = (int)src.size();
   m->ring = mix_mma_ring(N, r->ears, g->length, m->nsrc4, KS);
@@ -866,6 +879,7 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   cudaError_t e = cudaMalloc(&m->d_msrc, src.size() * sizeof(unsigned short));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mks, KS * sizeof(int2));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mrows, rinfo.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_mrowf, rowf.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mg, G.size());
   if (e == cudaSuccess) e = cudaMalloc(&m->d_ovh, (size_t)m->n_tiles * r->ears * m->ovh_pitch * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_tmax, (size_t)m->n_tiles * sizeof(float));
@@ -876,6 +890,8 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(m->d_mrows, rinfo.data(), rinfo.size() * sizeof(int), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(m->d_mg, G.data(), G.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(m->d_mrowf, rowf.data(), rowf.size() * sizeof(float), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host staging vectors die here
   if (e != cudaSuccess) {
     mma_plan_free(m);
@@ -957,7 +973,7 @@ int toep_mixer_destroy(toep_mixer* m) {
 
 int64_t toep_mixer_z_len(const toep_mixer* m) { return m ? m->zlen : -1; }
 int toep_mixer_path(const toep_mixer* m) { return m ? (m->mma ? TOEP_PATH_TENSOR : TOEP_PATH_WINDOW) : -1; }
-int toep_mixer_kernels(const toep_mixer* m) { return m ? (m->mma ? 4 : 3) : -1; }
+int toep_mixer_kernels(const toep_mixer* m) { return m ? (m->mma ? 5 : 3) : -1; }
 int64_t toep_mixer_out_len(const toep_mixer* m) { return m ? m->zlen + m->r->lf - 1 : -1; }
 
 int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s0, int32_t count, float* z,
@@ -994,6 +1010,7 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
     a.src = m->d_msrc;
     a.ks = m->d_mks;
     a.rows = m->d_mrows;
+    a.rowf = m->d_mrowf;
     a.g = m->d_mg;
     a.KS = m->KS;
     a.nsrc4 = m->nsrc4;

@@ -200,6 +200,7 @@ struct MixMmaArgs {
   const unsigned short* src;  // source rows in K-step order, each K-step padded to a multiple of 4 (tensor-map rows)
   const int2* ks;        // [KS] {first entry in src (multiple of 4), padded count}
   const int* rows;       // [KS][16] row r: offset | count << 6 | (gamma_d + 128) << 9
+  const float* rowf;     // [KS][16] main-pass multiplier 2^(sexp - gamma_d) of row r
   const unsigned char* g;  // [KS][hi, lo][canonical N x 16] fp16 of g * 2^gamma_d
   int KS;
   int nsrc4;             // entries of src (all K-steps, padded)
@@ -220,7 +221,7 @@ struct MixMmaArgs {
   const int* bad_count;
   int* nonfinite;
 };
-// main pass, bad-tile scan, fixup pass, overhang carry (4 launches)
+// main pass, bad-tile scan, fixup pass, overhang carry, z finite check (5 launches; 4 without the check)
 // tm: 2-D tensor map over the sources {T, rows}, box {kMixTile, 1} (tile::gather4 loads)
 cudaError_t launch_mix_mma(const MixMmaArgs& a, const CUtensorMap& tm, int* bad_list, int* bad_count, int sm_count,
                            cudaStream_t st);

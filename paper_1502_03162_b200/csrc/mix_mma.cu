@@ -110,7 +110,7 @@ __device__ __forceinline__ float p2f(int e) { return __int_as_float((127 + e) <<
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct MxSmem {
-  int ring, g, ebuf, src, rows, ksn, misc, bars, total;
+  int ring, g, ebuf, src, rows, rowf, ksn, misc, bars, total;
 };
 // Shared-memory layout; the source ring takes what the tables leave of the
 // 227 KB (ring = 0 asks for the ring size that fits, >= kMxMinRing slots).
@@ -126,6 +126,8 @@ __host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, in
   L.src = off;  // [nsrc4] source rows of the K-steps (uint16, 8-byte aligned groups of 4)
   off += ((nsrc4 + 7) & ~7) * 2;
   L.rows = off;  // [KS][16] row info
+  off += KS * 64;
+  L.rowf = off;  // [KS][16] main-pass row multipliers 2^(sexp - gamma_d)
   off += KS * 64;
   L.ksn = off;  // [KS] int2 {src offset, count}
   off += ((KS + 1) & ~1) * 8;
@@ -153,11 +155,19 @@ struct MxTiles {
   }
 };
 
+// tile scale exponent: the launch's in the main pass; in the fixup pass the
+// one that puts the tile's recorded max |A| (at the launch scale) into
+// [2^13, 2^14) -- integer arithmetic, so no intermediate under/overflows
 __device__ __forceinline__ int mx_tile_sexp(const MixMmaArgs& a, int j) {
   if (!a.bad_list) return a.sexp;
-  const float m = a.tile_max[j];  // unscaled max |Y_d 2^-gamma_d| of the tile
-  int s = m > 0.f ? 13 - ilogbf(m) : a.sexp;
-  return max(-100, min(100, s));
+  const float m = a.tile_max[j];
+  return m > 0.f ? a.sexp + 13 - ilogbf(m) : a.sexp;
+}
+// 2^e for any e: two exact factors (each clamped to the normal range, where
+// the value they scale would under/overflow anyway)
+__device__ __forceinline__ float2 p2f2(int e) {
+  const int e1 = max(-126, min(127, e >> 1)), e2 = max(-126, min(127, e - (e >> 1)));
+  return make_float2(p2f(e1), p2f(e2));
 }
 
 #ifndef TOEP_MIX_PROF
@@ -193,6 +203,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   float* s_bmax = reinterpret_cast<float*>(sm + L.misc);
   uint2* s_src4 = reinterpret_cast<uint2*>(sm + L.src);  // 4 x uint16 per gather
   int4* s_rows4 = reinterpret_cast<int4*>(sm + L.rows);
+  float4* s_rowf4 = reinterpret_cast<float4*>(sm + L.rowf);
   int2* s_ksn = reinterpret_cast<int2*>(sm + L.ksn);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
   uint64_t* src_full = bars;
@@ -237,7 +248,10 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   }
   // the K-step tables (identical for every tile) -> shared memory
   for (int i = tid; i < (a.nsrc4 >> 2); i += kMxThreads) s_src4[i] = __ldg(reinterpret_cast<const uint2*>(a.src) + i);
-  for (int i = tid; i < a.KS * 4; i += kMxThreads) s_rows4[i] = __ldg(reinterpret_cast<const int4*>(a.rows) + i);
+  for (int i = tid; i < a.KS * 4; i += kMxThreads) {
+    s_rows4[i] = __ldg(reinterpret_cast<const int4*>(a.rows) + i);
+    s_rowf4[i] = __ldg(reinterpret_cast<const float4*>(a.rowf) + i);
+  }
   for (int i = tid; i < a.KS; i += kMxThreads) s_ksn[i] = __ldg(a.ks + i);
   tmem_fence_before();
   __syncthreads();
@@ -359,17 +373,14 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
     long long seq = 0;
     int pos = 0, as = 0;
     unsigned aph = 0;
-    float chk0 = 0.f, chk1 = 0.f;
+    const bool fixup = a.bad_list != nullptr;
 #if TOEP_MIX_PROF
     _tp = clock64();
 #endif
     for (int i = 0;; ++i) {
       const int j = tiles.at(i);
       if (j < 0) break;
-      const long long t0 = (long long)j * kMixTile;
-      const bool valid = t0 + tt < a.T;
-      const int sexp = mx_tile_sexp(a, j);
-      const float S = p2f(sexp);
+      const int sexp = mx_tile_sexp(a, j);  // (samples past T arrive as zeros: TMA out-of-bounds fill)
       float amax = 0.f;
       for (int ks = 0; ks < KS; ++ks) {
         const int n = s_ksn[ks].y;
@@ -399,16 +410,23 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         if (lane == 0) mbar_arrive(&src_empty[seq % kMxKR]);
         PROF_MARK(4);
         unsigned hw[4], lw[4];
+        float mul[8];
+        if (!fixup) {  // 2^(sexp - gamma_d), precomputed
+          const float4 m0 = s_rowf4[4 * ks + 2 * half], m1 = s_rowf4[4 * ks + 2 * half + 1];
+          mul[0] = m0.x; mul[1] = m0.y; mul[2] = m0.z; mul[3] = m0.w;
+          mul[4] = m1.x; mul[5] = m1.y; mul[6] = m1.z; mul[7] = m1.w;
+        } else {  // the tile's own exponent: two exact factors per row
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const float2 f = p2f2(sexp - (((ri[r] >> 9) & 0xff) - 128));
+            v[r] *= f.x;
+            mul[r] = f.y;
+          }
+        }
 #pragma unroll
         for (int r = 0; r < 8; r += 2) {
-          // Y_d 2^-gamma_d  (row multiplier 2^-gamma_d from the row's exponent field)
-          float x0 = valid ? v[r] * __int_as_float((255 - ((ri[r] >> 9) & 0xff)) << 23) : 0.f;
-          float x1 = valid ? v[r + 1] * __int_as_float((255 - ((ri[r + 1] >> 9) & 0xff)) << 23) : 0.f;
-          chk0 = fmaf(x0, 0.f, chk0);
-          chk1 = fmaf(x1, 0.f, chk1);
+          const float x0 = v[r] * mul[r], x1 = v[r + 1] * mul[r + 1];
           amax = fmaxf(amax, fmaxf(fabsf(x0), fabsf(x1)));
-          x0 *= S;
-          x1 *= S;
           const unsigned h = mx_h2(x0, x1);
           const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
           hw[r / 2] = h;
@@ -446,7 +464,6 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         named_sync(1, 32 * kMxBuildWarps);
       }
     }
-    if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk0 + chk1)) && lane == 0) atomicOr(a.nonfinite, 1);
   } else if (warp >= 4 + kMxBuildWarps) {
     // ===== epilogue: W -> overlap-add -> z (one warp per row block x lane quarter) =====
     const int ew = warp - 4 - kMxBuildWarps;
@@ -507,7 +524,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       named_sync(2, 32 * kMxEpiWarps);
       // combine the 8 windows (fixed order): position P of the tile's 256 + K - 1
       const long long t0 = (long long)j * kMixTile;
-      const float inv = p2f(-mx_tile_sexp(a, j));
+      const float2 inv = p2f2(-mx_tile_sexp(a, j));
       const int npos = kMixTile + K - 1;
       const int et = tid - 32 * (4 + kMxBuildWarps);
       for (int idx = et; idx < ears * npos; idx += 32 * kMxEpiWarps) {
@@ -518,7 +535,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           const int b = 128 * (w >> 2) + 32 * (w & 3);
           if (P >= b && P < b + win) acc += eb[(w * ears + e) * win + (P - b)];
         }
-        acc *= inv;
+        acc = acc * inv.x * inv.y;
         if (P < kMixTile) {
           if (t0 + P < a.zlen) a.z[(long long)e * a.z_pitch + t0 + P] = acc;
         } else {
@@ -539,32 +556,18 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   if (warp == 3) tmem_dealloc<512>(tbase);
 }
 
-// bad-tile list for the fixup pass (one CTA)
-__global__ void __launch_bounds__(1024) k_mix_scan(const float* __restrict__ tile_max, int n_tiles, int sexp,
+// bad-tile list for the fixup pass (one CTA): tiles whose max |A| at the
+// launch scale left the fp16-safe window [2^-3, 2^15] -- the hi half would
+// overflow, or the lo half of the tile's largest values would not be a
+// normal fp16 number; all-zero tiles are exact at any scale
+__global__ void __launch_bounds__(1024) k_mix_scan(const float* __restrict__ tile_max, int n_tiles,
                                                     int* __restrict__ list, int* __restrict__ count) {
-  __shared__ float s_red[32];
-  float m = 0.f;
-  for (int j = threadIdx.x; j < n_tiles; j += blockDim.x) {
-    const float v = tile_max[j];
-    if (isfinite(v)) m = fmaxf(m, v);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
   if (threadIdx.x == 0) *count = 0;
   __syncthreads();
-  float g = 0.f;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) g = fmaxf(g, s_red[w]);
-  const float S = ldexpf(1.f, sexp);
   for (int j = threadIdx.x; j < n_tiles; j += blockDim.x) {
-    const float v = tile_max[j];
-    if (!isfinite(v) || v == 0.f) continue;
-    const float s = v * S;
-    // fp16-safe window of the scaled tile: |x| <= 2^15 (no overflow of the
-    // hi half) and, for a tile that matters (>= 2^-24 of the loudest), >= 2^-3
-    // (the lo half stays a normal fp16 number for the tile's largest values)
-    const bool bad = s > 32768.f || (s < 0.125f && v >= g * 5.9604645e-8f);
-    if (bad) list[atomicAdd(count, 1)] = j;
+    const float s = tile_max[j];
+    if (!isfinite(s) || s == 0.f) continue;  // non-finite input: reported by the z check, not re-rendered
+    if (s > 32768.f || s < 0.125f) list[atomicAdd(count, 1)] = j;
   }
 }
 
@@ -584,6 +587,23 @@ __global__ void k_mix_carry(float* __restrict__ z, long long z_pitch, long long 
     float* zp = z + (long long)e * z_pitch + pos;
     *zp = (j + 1 < n_tiles ? *zp : 0.f) + v;
   }
+}
+
+// fused input check of the tensor mixdown (the reference's DataError for
+// non-finite samples, engine/__init__.py:162-165): a non-finite source sample
+// makes its tile's z non-finite (sums, fp16 halves and products propagate
+// inf/NaN), so the finished z is checked instead of every source sample
+// (23 MB instead of 47 GB at config 5)
+__global__ void k_mix_zcheck(const float* __restrict__ z, long long z_pitch, long long zlen, int ears,
+                             int* __restrict__ nonfinite) {
+  bool bad = false;
+  for (int e = 0; e < ears; ++e) {
+    const float* ze = z + (long long)e * z_pitch;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < zlen;
+         t += (long long)gridDim.x * blockDim.x)
+      bad |= !isfinite(ze[t]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
 
 int mix_mma_nr(int K) { return (32 + K - 1 + 31) / 32; }
@@ -621,12 +641,11 @@ cudaError_t launch_mix_mma(const MixMmaArgs& a_in, const CUtensorMap& tm, int* b
   };
   cudaError_t e = go(a);
   if (e != cudaSuccess) return e;
-  k_mix_scan<<<1, 1024, 0, st>>>(a.tile_max, a.n_tiles, a.sexp, bad_list, bad_count);
+  k_mix_scan<<<1, 1024, 0, st>>>(a.tile_max, a.n_tiles, bad_list, bad_count);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   MixMmaArgs f = a;
   f.bad_list = bad_list;
   f.bad_count = bad_count;
-  f.nonfinite = nullptr;
   e = go(f);
   if (e != cudaSuccess) return e;
   const int nov = a.K - 1;
@@ -635,6 +654,11 @@ cudaError_t launch_mix_mma(const MixMmaArgs& a_in, const CUtensorMap& tm, int* b
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sm_count * 8);
     k_mix_carry<<<std::max(blocks, 1), 256, 0, st>>>(a.z, a.z_pitch, a.zlen, a.ovh, a.ovh_pitch, a.n_tiles, a.ears,
                                                       nov);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (a.nonfinite) {
+    const int blocks = (int)std::min<long long>((a.zlen + 255) / 256, (long long)sm_count * 8);
+    k_mix_zcheck<<<std::max(blocks, 1), 256, 0, st>>>(a.z, a.z_pitch, a.zlen, a.ears, a.nonfinite);
     e = cudaGetLastError();
   }
   return e;

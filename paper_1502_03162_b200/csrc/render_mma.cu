@@ -398,13 +398,28 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       if (e != cur_e)
         for (int i = bt; i < a.lf_pad; i += kMmaBuilders) s_f[i] = a.f[(long long)e * a.lf_pad + i];
       cur_e = e;
+      float ymx = 0.f;
       for (int i = bt; i < YL; i += kMmaBuilders) {
         const long long t = y0 + i;
         const float v = (t >= 0 && t < a.nx) ? __ldg(a.x + t) : 0.f;
         chk = fmaf(v, 0.f, chk);
+        ymx = fmaxf(ymx, fabsf(v));
         s_y[i] = v;
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ymx = fmaxf(ymx, __shfl_xor_sync(0xffffffffu, ymx, o));
+      if (lane == 0) s_red[8 + warp - 2] = ymx;
       builders_sync();
+      // a tile of tiny (e.g. fp32-subnormal) input is scaled up by 2^pexp before
+      // the FIR, so stage 1 keeps full fp32 precision; pexp joins the tile exponent
+      ymx = 0.f;
+      for (int w = 0; w < kMmaBuilderWarps; ++w) ymx = fmaxf(ymx, s_red[8 + w]);
+      const int pexp = (ymx > 0.f && ymx < 0x1p-64f) ? -ilogbf(ymx) : 0;
+      if (pexp) {
+        const float p1 = exp2i(pexp / 2), p2 = exp2i(pexp - pexp / 2);
+        for (int i = bt; i < YL; i += kMmaBuilders) s_y[i] = s_y[i] * p1 * p2;
+        builders_sync();
+      }
       float mx = 0.f;
       for (int i = bt; i < YF; i += kMmaBuilders) {
         float acc = 0.f;
@@ -425,7 +440,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const float sc1 = exp2i(sexp / 2), sc2 = exp2i(sexp - sexp / 2);
       if (bt == 0) {
         PW(5, mbar_wait_sleep(&sc_empty[nitem & 1], (unsigned)(((nitem >> 1) & 1) ^ 1)));
-        s_sc[nitem & 1] = __int_as_float(sexp);
+        s_sc[nitem & 1] = __int_as_float(sexp + pexp);
         mbar_arrive(&sc_full[nitem & 1]);
       }
       if (ring) {

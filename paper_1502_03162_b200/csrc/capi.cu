@@ -376,9 +376,32 @@ int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const f
   if (length < 1 || length > (1LL << 30)) return fail(TOEP_ERR_INVALID, "bad filter length");
   if (nnz < 0 || (nnz > 0 && (!indices || !values))) return fail(TOEP_ERR_INVALID, "bad tap arrays");
   cudaStream_t st = S(stream);
-  const int64_t row_ptr[2] = {0, nnz};
+  // the reference kernel takes the taps in any order, repeated offsets adding
+  // up (_kernels.pyx:38-43): sort by offset and merge repeats (in double)
+  // into the strictly increasing form the tap tables hold
+  std::vector<int64_t> ci;
+  std::vector<float> cv;
+  {
+    std::vector<int64_t> ord(nnz);
+    for (int64_t k = 0; k < nnz; ++k) {
+      if (indices[k] < 0 || indices[k] >= length)
+        return fail(TOEP_ERR_INVALID, "indices must lie in [0, %lld)", (long long)length);
+      if (!std::isfinite(values[k])) return fail(TOEP_ERR_INVALID, "values must be finite");
+      ord[k] = k;
+    }
+    std::stable_sort(ord.begin(), ord.end(), [indices](int64_t x, int64_t y2) { return indices[x] < indices[y2]; });
+    for (int64_t k = 0; k < nnz;) {
+      double acc = 0.0;
+      int64_t q = k;
+      while (q < nnz && indices[ord[q]] == indices[ord[k]]) acc += values[ord[q++]];
+      ci.push_back(indices[ord[k]]);
+      cv.push_back((float)acc);
+      k = q;
+    }
+  }
+  const int64_t row_ptr[2] = {0, (int64_t)ci.size()};
   toep_taps* t = nullptr;
-  int rc = taps_build(1, (int32_t)length, row_ptr, indices, values, true, st, &t);
+  int rc = taps_build(1, (int32_t)length, row_ptr, ci.data(), cv.data(), true, st, &t);
   if (rc != TOEP_OK) return rc;
   rc = reflect_rows(t, 0, 1, t->d_rowpairs, t->d_rowpnnz, y, ny, out, 0, st);
   toep_taps_destroy(t);

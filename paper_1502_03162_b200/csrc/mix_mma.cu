@@ -116,6 +116,7 @@ struct MxSmem {
 // 227 KB (ring = 0 asks for the ring size that fits, >= kMxMinRing slots).
 constexpr int kMxSmemMax = 227 * 1024 - 1024;  // static shared memory + slack
 constexpr int kMxMinRing = 2 * kMixKsSrcs;      // 1 KB slots (two full K-steps)
+constexpr int kMxSlack = kMixRowSrcs - 1;       // slots past the ring end a row's unconditional loads may touch
 __host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, int KS, int ring) {
   MxSmem L{};
   int off = 0;
@@ -137,8 +138,8 @@ __host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, in
   off += (2 * kMxKR + 2 * kMxGR + 2 * kMxAR + 2) * 8;
   off = (off + 127) & ~127;
   L.ring = off;
-  if (ring <= 0) ring = (kMxSmemMax - off) / kMxSlotBytes;
-  off += ring * kMxSlotBytes;
+  if (ring <= 0) ring = (kMxSmemMax - off) / kMxSlotBytes - kMxSlack;
+  off += (ring + kMxSlack) * kMxSlotBytes;
   L.total = off;
   return L;
 }
@@ -172,6 +173,14 @@ __device__ __forceinline__ float2 p2f2(int e) {
 
 #ifndef TOEP_MIX_PROF
 #define TOEP_MIX_PROF 0
+#endif
+// builders poll their barriers (short waits on the critical path); every
+// other role suspends in try_wait (a polling warp steals issue slots from the
+// builders: 8 spinning epilogue warps were ~20% of all issued instructions)
+#if defined(TOEP_MIX_SLEEPALL) && TOEP_MIX_SLEEPALL
+#define MX_BWAIT mbar_wait_sleep
+#else
+#define MX_BWAIT mbar_wait
 #endif
 #if TOEP_MIX_PROF
 #define PROF_WAIT(slot, ...)         \
@@ -285,7 +294,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           const int n = info.y;  // multiple of 4
           const int skip = pos + n > RING ? RING - pos : 0;
           while (seq - fseq >= kMxKR || held + skip + n > RING) {
-            PROF_WAIT(0, mbar_wait(&src_empty[fseq % kMxKR], (unsigned)((fseq / kMxKR) & 1)));
+            PROF_WAIT(0, mbar_wait_sleep(&src_empty[fseq % kMxKR], (unsigned)((fseq / kMxKR) & 1)));
             held -= hold[fseq % kMxKR];
             ++fseq;
           }
@@ -338,8 +347,8 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         cph ^= 1u;
         tmem_fence_after();
         for (int ks = 0; ks < KS; ++ks) {
-          PROF_WAIT(0, mbar_wait(&g_full[gs], gph));
-          PROF_WAIT(1, mbar_wait(&a_full[as], aph));
+          PROF_WAIT(0, mbar_wait_sleep(&g_full[gs], gph));
+          PROF_WAIT(1, mbar_wait_sleep(&a_full[as], aph));
           tmem_fence_after();
           const unsigned bh = sg + (unsigned)(gs * gbytes), bl = bh + (unsigned)(N * 32);
 #pragma unroll
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
         if (pos + n > RING) pos = 0;
         PROF_MARK(3);
-        PROF_WAIT(0, mbar_wait(&src_full[seq % kMxKR], (unsigned)((seq / kMxKR) & 1)));
+        PROF_WAIT(0, MX_BWAIT(&src_full[seq % kMxKR], (unsigned)((seq / kMxKR) & 1)));
         PROF_MARK(7);
         const float* base = ring + pos * kMixTile + tt;
         float v[8];
@@ -433,7 +442,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           lw[r / 2] = mx_h2(x0 - hf.x, x1 - hf.y);
         }
         PROF_MARK(5);
-        PROF_WAIT(1, mbar_wait(&a_empty[as], aph ^ 1u));
+        PROF_WAIT(1, MX_BWAIT(&a_empty[as], aph ^ 1u));
         PROF_MARK(7);
         tmem_fence_after();
         const unsigned ta = ta0 + (unsigned)(32 * as);
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         R0[k] = 0.f;
         R1[k] = 0.f;
       }
-      PROF_WAIT(0, mbar_wait(acc_full, cph));
+      PROF_WAIT(0, mbar_wait_sleep(acc_full, cph));
       cph ^= 1u;
       tmem_fence_after();
 #pragma unroll
@@ -611,7 +620,7 @@ int mix_mma_nr(int K) { return (32 + K - 1 + 31) / 32; }
 // ring slots left by the tables (0 if the tables do not leave kMxMinRing slots)
 int mix_mma_ring(int N, int ears, int K, int nsrc4, int KS) {
   const int nr = mix_mma_nr(K) <= 5 ? 5 : 8;
-  const int ring = (kMxSmemMax - mx_smem(N, ears, nr, nsrc4, KS, 1).ring) / kMxSlotBytes;
+  const int ring = (kMxSmemMax - mx_smem(N, ears, nr, nsrc4, KS, 1).ring) / kMxSlotBytes - kMxSlack;
   return ring >= kMxMinRing ? ring : 0;
 }
 

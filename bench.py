@@ -834,6 +834,33 @@ def _nccl_init_lines(path):
         return []
 
 
+def dry_run(args, world, rank):
+    """The multi-rank launch path without a GPU: self-spawn under torchrun,
+    one process per "GPU", gloo rendezvous, each rank's share of the cfg5
+    sources by direction (dist.MixShard's partition), gathered on rank 0."""
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _spawn(args.gpus)
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
+    from paper_1502_03162_b200 import dist as tdist, synth
+    cfg = synth.CONFIGS["cfg5"]
+    sd = synth.source_directions(cfg.sources, cfg.dirs, seed=5)
+    mine = tdist.partition_by_direction(sd, world)[rank]
+    share = {"rank": rank, "sources": int(mine.size), "directions": int(np.unique(sd[mine]).size),
+             "first": int(mine[0]) if mine.size else -1}
+    shares = [share]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        shares = [None] * world
+        dist.all_gather_object(shares, share)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "config": workload_config("cfg5", world),
+                          "shares": shares}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -844,9 +871,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused", action="store_true", help="skip the cfg2 fused_render object at N=1")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: launch the ranks (gloo), partition the cfg5 sources, print the plan")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = _dist()
+    if args.dry_run:
+        return dry_run(args, world, rank)
 
     if args.impl == "reference":
         return run_reference(args, world, rank)

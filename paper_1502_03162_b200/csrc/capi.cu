@@ -810,55 +810,64 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   std::vector<int> ord(count);
   for (int i = 0; i < count; ++i) ord[i] = i;
   std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
+  // rows: a direction's sources in groups of kMixRowSrcs, the remainder in one
+  // smaller row; K-steps hold 16 rows of ONE size class c (4, 3, 2, 1 sources),
+  // so a K-step is 16c consecutive ring slots, row r at slots [c r, c r + c)
+  // (the builders' loads use compile-time offsets, no per-row predicates);
+  // only the last K-step of a class has padding rows (out-of-range source
+  // rows: TMA fills their slots with zeros, no memory traffic)
   struct Row { int d, first, cnt; };
-  std::vector<Row> rows;
+  std::vector<Row> byc[kMixRowSrcs + 1];
   for (int p = 0; p < count;) {
     int q = p;
     while (q < count && dir[ord[q]] == dir[ord[p]]) ++q;
-    for (int a = p; a < q; a += kMixRowSrcs) rows.push_back({dir[ord[p]], a, std::min(kMixRowSrcs, q - a)});
+    for (int a2 = p; a2 < q; a2 += kMixRowSrcs) {
+      const int c = std::min(kMixRowSrcs, q - a2);
+      byc[c].push_back({dir[ord[p]], a2, c});
+    }
     p = q;
   }
   std::vector<int2> ks;
-  std::vector<int> rinfo;    // [KS][16] offset | count << 6 | (gamma_d + 128) << 9
+  std::vector<int> rinfo;    // [KS][16] (gamma_d + 128) << 9 (the fixup pass scales per row)
   std::vector<float> rowf;   // [KS][16] main-pass multipliers 2^(sexp - gamma_d)
   bool clamped = false;
   std::vector<int> ks_dirs;  // [KS][16] direction per row (-1 empty), gamma_d
-  std::vector<unsigned short> src;  // K-step source lists, each padded to a multiple of 4 with an out-of-range row
-  for (size_t i = 0; i < rows.size();) {
-    const int start = rows[i].first;
-    int nr = 0, ns = 0;
-    while (i + nr < rows.size() && nr < 16 && ns + rows[i + nr].cnt <= kMixKsSrcs) ns += rows[i + nr++].cnt;
-    const int ns4 = (ns + 3) & ~3;
-    ks.push_back(make_int2((int)src.size(), ns4));
-    for (int k = 0; k < ns4; ++k) src.push_back((unsigned short)(k < ns ? ord[start + k] : count));
-    for (int k = 0; k < 16; ++k) {
-      if (k < nr) {
-        const Row& w = rows[i + k];
-        float mx = 0.f;
-        for (int e = 0; e < r->ears; ++e) {
-          const int row = e * r->dirs + w.d;
-          for (int t = 0; t < m->h_nnz[row]; ++t) {
-            float v;
-            memcpy(&v, &m->h_taps[(size_t)row * g->tap_stride + t].y, 4);
-            mx = std::max(mx, std::fabs(v));
+  std::vector<unsigned short> src;  // K-step source lists: 16 rows x c entries
+  for (int c = kMixRowSrcs; c >= 1; --c) {
+    const std::vector<Row>& rows = byc[c];
+    for (size_t i = 0; i < rows.size(); i += 16) {
+      const int nr = (int)std::min<size_t>(16, rows.size() - i);
+      ks.push_back(make_int2((int)src.size(), 16 * c));
+      for (int k = 0; k < 16; ++k)
+        for (int u = 0; u < c; ++u) src.push_back((unsigned short)(k < nr ? ord[rows[i + k].first + u] : count));
+      for (int k = 0; k < 16; ++k) {
+        if (k < nr) {
+          const Row& w = rows[i + k];
+          float mx = 0.f;
+          for (int e = 0; e < r->ears; ++e) {
+            const int row = e * r->dirs + w.d;
+            for (int t = 0; t < m->h_nnz[row]; ++t) {
+              float v;
+              memcpy(&v, &m->h_taps[(size_t)row * g->tap_stride + t].y, 4);
+              mx = std::max(mx, std::fabs(v));
+            }
           }
+          int gam = mx > 0.f ? 13 - std::ilogb(mx) : 0;
+          gam = std::max(-126, std::min(126, gam));
+          rinfo.push_back((gam + 128) << 9);
+          const int em = m->sexp - gam;
+          clamped |= em < -126 || em > 127;
+          rowf.push_back(std::ldexp(1.f, std::max(-126, std::min(127, em))));
+          ks_dirs.push_back(w.d);
+          ks_dirs.push_back(gam);
+        } else {
+          rinfo.push_back(128 << 9);  // padding row
+          rowf.push_back(0.f);
+          ks_dirs.push_back(-1);
+          ks_dirs.push_back(0);
         }
-        int gam = mx > 0.f ? 13 - std::ilogb(mx) : 0;
-        gam = std::max(-126, std::min(126, gam));
-        rinfo.push_back((w.first - start) | (w.cnt << 6) | ((gam + 128) << 9));
-        const int em = m->sexp - gam;
-        clamped |= em < -126 || em > 127;
-        rowf.push_back(std::ldexp(1.f, std::max(-126, std::min(127, em))));
-        ks_dirs.push_back(w.d);
-        ks_dirs.push_back(gam);
-      } else {
-        rinfo.push_back(128 << 9);  // empty row
-        rowf.push_back(0.f);
-        ks_dirs.push_back(-1);
-        ks_dirs.push_back(0);
       }
     }
-    i += nr;
   }
   const int KS = (int)ks.size();
   const int N = m->N, KP = m->KP;

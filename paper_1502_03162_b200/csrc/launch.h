@@ -189,7 +189,7 @@ cudaError_t launch_ear_pair_taps(const int2* rows, int dirs, int ears, int strid
 // Tensor-core mixdown (mix_mma.cu): W[t][(e,o)] = sum_d Y_d[t] G[d][(e,o)] on
 // tcgen05 (M = 128 time rows, K = 16 direction rows per step, N = ears x KP),
 // then z_e[t] = sum_o W[t-o][(e,o)].  The host plans K-steps of up to 16 rows
-// (a row = up to kMixRowSrcs sources of one direction, <= kMixKsSrcs per step).
+// (a row = up to kMixRowSrcs sources of one direction; one row size per K-step).
 constexpr int kMixTile = 256;     // samples per tile (two 128-row blocks of the MMA)
 constexpr int kMixRowSrcs = 4;    // sources per direction row
 constexpr int kMixKsSrcs = 64;    // sources per K-step

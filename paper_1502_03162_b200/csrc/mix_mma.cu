@@ -107,6 +107,22 @@ __device__ __forceinline__ unsigned mx_h2(float a, float b) {
   return *reinterpret_cast<const unsigned*>(&h);
 }
 __device__ __forceinline__ float p2f(int e) { return __int_as_float((127 + e) << 23); }  // 2^e, e in [-126, 127]
+
+// the direction sums of 8 rows of C slices each: slot (C r + k) of the row
+// block, compile-time offsets (all 8 C loads issue before the adds)
+template <int C>
+__device__ __forceinline__ void mx_row_sums(const float* __restrict__ base, float (&v)[8]) {
+  float L[8 * C];
+#pragma unroll
+  for (int i = 0; i < 8 * C; ++i) L[i] = base[i * kMixTile];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    if constexpr (C == 4) v[r] = (L[4 * r] + L[4 * r + 2]) + (L[4 * r + 1] + L[4 * r + 3]);
+    else if constexpr (C == 3) v[r] = (L[3 * r] + L[3 * r + 2]) + L[3 * r + 1];
+    else if constexpr (C == 2) v[r] = L[2 * r] + L[2 * r + 1];
+    else v[r] = L[r];
+  }
+}
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct MxSmem {
@@ -116,7 +132,6 @@ struct MxSmem {
 // 227 KB (ring = 0 asks for the ring size that fits, >= kMxMinRing slots).
 constexpr int kMxSmemMax = 227 * 1024 - 1024;  // static shared memory + slack
 constexpr int kMxMinRing = 2 * kMixKsSrcs;      // 1 KB slots (two full K-steps)
-constexpr int kMxSlack = kMixRowSrcs - 1;       // slots past the ring end a row's unconditional loads may touch
 __host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, int KS, int ring) {
   MxSmem L{};
   int off = 0;
@@ -138,8 +153,8 @@ __host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, in
   off += (2 * kMxKR + 2 * kMxGR + 2 * kMxAR + 2) * 8;
   off = (off + 127) & ~127;
   L.ring = off;
-  if (ring <= 0) ring = (kMxSmemMax - off) / kMxSlotBytes - kMxSlack;
-  off += (ring + kMxSlack) * kMxSlotBytes;
+  if (ring <= 0) ring = (kMxSmemMax - off) / kMxSlotBytes;
+  off += ring * kMxSlotBytes;
   L.total = off;
   return L;
 }
@@ -392,28 +407,23 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       const int sexp = mx_tile_sexp(a, j);  // (samples past T arrive as zeros: TMA out-of-bounds fill)
       float amax = 0.f;
       for (int ks = 0; ks < KS; ++ks) {
-        const int n = s_ksn[ks].y;
+        const int n = s_ksn[ks].y;  // 16 rows x c slots (c = sources per row, one size class per K-step)
         const int4 ra = s_rows4[4 * ks + 2 * half], rbv = s_rows4[4 * ks + 2 * half + 1];  // this warp's 8 rows
         const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
         if (pos + n > RING) pos = 0;
         PROF_MARK(3);
         PROF_WAIT(0, MX_BWAIT(&src_full[seq % kMxKR], (unsigned)((seq / kMxKR) & 1)));
         PROF_MARK(7);
-        const float* base = ring + pos * kMixTile + tt;
         float v[8];
-#pragma unroll
-        for (int h4 = 0; h4 < 2; ++h4) {  // 16 predicated loads in flight, then the adds
-          float L0[16];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int rr = 4 * h4 + r;
-            const int cnt = (ri[rr] >> 6) & 7;
-            const float* p = base + (ri[rr] & 63) * kMixTile;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) L0[4 * r + k] = cnt > k ? p[k * kMixTile] : 0.f;
+        {
+          const int c = n >> 4;
+          const float* base = ring + (pos + 8 * c * half) * kMixTile + tt;  // this warp's first row
+          switch (c) {
+            case 4: mx_row_sums<4>(base, v); break;
+            case 3: mx_row_sums<3>(base, v); break;
+            case 2: mx_row_sums<2>(base, v); break;
+            default: mx_row_sums<1>(base, v); break;
           }
-#pragma unroll
-          for (int r = 0; r < 4; ++r) v[4 * h4 + r] = (L0[4 * r] + L0[4 * r + 2]) + (L0[4 * r + 1] + L0[4 * r + 3]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&src_empty[seq % kMxKR]);
@@ -620,7 +630,7 @@ int mix_mma_nr(int K) { return (32 + K - 1 + 31) / 32; }
 // ring slots left by the tables (0 if the tables do not leave kMxMinRing slots)
 int mix_mma_ring(int N, int ears, int K, int nsrc4, int KS) {
   const int nr = mix_mma_nr(K) <= 5 ? 5 : 8;
-  const int ring = (kMxSmemMax - mx_smem(N, ears, nr, nsrc4, KS, 1).ring) / kMxSlotBytes - kMxSlack;
+  const int ring = (kMxSmemMax - mx_smem(N, ears, nr, nsrc4, KS, 1).ring) / kMxSlotBytes;
   return ring >= kMxMinRing ? ring : 0;
 }
 

@@ -189,6 +189,9 @@ __device__ __forceinline__ float2 p2f2(int e) {
 #ifndef TOEP_MIX_PROF
 #define TOEP_MIX_PROF 0
 #endif
+#ifndef TOEP_MIX_PRODUCTS
+#define TOEP_MIX_PRODUCTS 3
+#endif
 // builders poll their barriers (short waits on the critical path); every
 // other role suspends in try_wait (a polling warp steals issue slots from the
 // builders: 8 spinning epilogue warps were ~20% of all issued instructions)
@@ -371,8 +374,12 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
             const unsigned d = tbase + (unsigned)(rb * N);
             const unsigned ah = tbase + (unsigned)(kMxACol + 32 * as + 16 * rb), al = ah + 8;
             mx_mma(d, ah, mx_sdesc(bh), idesc, ks > 0);
+#if TOEP_MIX_PRODUCTS > 1  // experiment knob: 3 products are needed for fp32 accuracy
             mx_mma(d, ah, mx_sdesc(bl), idesc, 1);
+#endif
+#if TOEP_MIX_PRODUCTS > 2
             mx_mma(d, al, mx_sdesc(bh), idesc, 1);
+#endif
           }
           mx_commit(&a_empty[as]);
           mx_commit(&g_empty[gs]);

@@ -24,8 +24,12 @@
  * Threading (as the reference's plans and renderers, engine/__init__.py:16-18):
  * distinct objects may be used concurrently from any thread / stream; the
  * calls on one renderer, mixer or streamer must be ordered (one stream at a
- * time) -- they own device scratch (check flag, tensor-map cache, the mix
- * item counter, the stream history).  Read-only queries are always safe.
+ * time) -- they own device scratch (tensor-map caches, the fill launch's side
+ * stream, the mix plan and item counter, the stream history).  Mixers and
+ * streamers made from one renderer report non-finite input through that
+ * renderer's flag (toep_renderer_check): order them with the renderer, or
+ * give each its own renderer (the Python layer does).  Read-only queries are
+ * always safe.
  */
 #ifndef TOEP_B200_H
 #define TOEP_B200_H
@@ -57,8 +61,9 @@ int toep_sm_count(int* out);
 int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps, float* out, int64_t* macs,
                     void* stream);
 
-/* Sparse taps given as HOST arrays (indices strictly increasing in
- * [0, length), values finite); out[0 .. ny+length-1) on the device.
+/* Sparse taps given as HOST arrays (indices in [0, length) in any order,
+ * repeated indices adding up -- as the reference kernel accumulates them;
+ * values finite); out[0 .. ny+length-1) on the device.
  * ref: _kernels.pyx:28-44 (conv_sparse).  *macs = nnz*ny. */
 int toep_conv_sparse(const float* y, int64_t ny, const int64_t* indices, const float* values, int64_t nnz,
                      int64_t length, float* out, int64_t* macs, void* stream);
@@ -144,7 +149,9 @@ int64_t toep_mixer_z_len(const toep_mixer* m);   /* T + length - 1 */
 int64_t toep_mixer_out_len(const toep_mixer* m); /* T + lf + length - 2 */
 /* z[e][t] = sum over sources s in [s0, s0+count) of (y_s * g_{e,dir(s)})[t]
  * (reflection first; linear, so partial sums from several calls or ranks add).
- * y: source s at y + (s - s0) * y_pitch. */
+ * y: source s at y + (s - s0) * y_pitch, 16-byte aligned, y_pitch % 4 == 0.
+ * Writes z[e][0 .. z_len) (no accumulation into z).  A non-finite source
+ * sample sets the renderer's non-finite flag (tensor path: detected on z). */
 int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s0, int32_t count, float* z,
                        int64_t z_pitch, void* stream);
 /* Kernel toep_mixer_partial uses: TOEP_PATH_TENSOR (split-fp16 GEMM over

@@ -106,17 +106,30 @@ def device_sources(S: int, T: int, seed: int = 0, device: str = "cuda", out=None
     return out
 
 
+SOURCE_CHUNK = 256  # rows drawn per generator call by device_sources_indexed
+
+
 def device_sources_indexed(indices, T: int, seed: int = 0, device: str = "cuda", out=None):
-    """Rows of the global source set: row i holds source ``indices[i]`` drawn on
-    the device from its own Philox stream (seed, global index), so a sharded
-    run renders exactly the sources a one-GPU run renders."""
+    """Rows of the global source set: row i holds source ``indices[i]``, drawn
+    on the device (Philox) as part of its chunk of SOURCE_CHUNK consecutive
+    global sources, each chunk from its own seeded stream -- so a sharded run
+    renders exactly the sources a one-GPU run renders, whatever the split,
+    with one generator call per chunk touched."""
     import torch
 
     idx = np.asarray(indices, dtype=np.int64)
     if out is None:
         out = torch.empty((idx.size, T), device=device, dtype=torch.float32)
+    if idx.size == 0:
+        return out
     g = torch.Generator(device=device)
-    for i, s in enumerate(idx):
-        g.manual_seed(int(seed) * 1_000_003 + int(s))
-        out[i].normal_(generator=g)
+    chunks = np.unique(idx // SOURCE_CHUNK)
+    buf = torch.empty((SOURCE_CHUNK, T), device=device, dtype=torch.float32)
+    pos = torch.as_tensor(np.arange(idx.size), device=device)
+    for c in chunks:
+        g.manual_seed(int(seed) * 1_000_003 + int(c))
+        buf.normal_(generator=g)
+        sel = np.flatnonzero(idx // SOURCE_CHUNK == c)
+        out[pos[torch.as_tensor(sel, device=device)]] = buf[torch.as_tensor(idx[sel] - c * SOURCE_CHUNK,
+                                                                            device=device)]
     return out

@@ -72,6 +72,7 @@ constexpr int kMxAR = 3;       // A slots in TMEM (32 columns each: row block 0 
 constexpr int kMxACol = 416;   // first A-slot column (accumulators: 2 row blocks x N <= 416)
 constexpr int kMxSlotBytes = kMixTile * 4;
 constexpr int kMxWindows = 8;  // overlap-add windows per tile: (row block, lane quarter)
+constexpr int kMxGroupKs = 96; // K-steps accumulated in TMEM before a drain (bounds the accumulation error)
 
 __device__ __forceinline__ uint64_t mx_sdesc(unsigned saddr) {
   // canonical K-major, SWIZZLE_NONE: LBO (K halves) 128 B, SBO (8-row groups) 256 B, version 1
@@ -161,14 +162,20 @@ __host__ __device__ inline MxSmem mx_smem(int N, int ears, int nr, int nsrc4, in
 
 // tile sequence of this CTA: a contiguous range (main pass) or its share of
 // the bad-tile list (fixup pass)
+// Work units are (tile, K-step group): a tile whose K-steps exceed
+// kMxGroupKs is accumulated in groups, each drained into z (the first group
+// stores, later ones add) -- the tensor core's fp32 accumulation error grows
+// with the accumulation count, so this bounds it for any source count.
 struct MxTiles {
   const int* list;
-  int j0, j1, cnt;
-  __device__ int at(int i) const {
-    if (!list) return j0 + i < j1 ? j0 + i : -1;
-    const int k = i * (int)gridDim.x + (int)blockIdx.x;
+  int j0, j1, cnt, ng;
+  __device__ int tile_of(int t) const {
+    if (!list) return j0 + t < j1 ? j0 + t : -1;
+    const int k = t * (int)gridDim.x + (int)blockIdx.x;
     return k < cnt ? list[k] : -1;
   }
+  __device__ int at(int i) const { return tile_of(i / ng); }  // unit i -> tile (-1: done)
+  __device__ int group(int i) const { return i % ng; }
 };
 
 // tile scale exponent: the launch's in the main pass; in the fixup pass the
@@ -290,7 +297,9 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   tiles.j0 = (int)((long long)a.n_tiles * blockIdx.x / gridDim.x);
   tiles.j1 = (int)((long long)a.n_tiles * (blockIdx.x + 1) / gridDim.x);
   tiles.cnt = a.bad_list ? *a.bad_count : 0;
+  tiles.ng = (a.KS + kMxGroupKs - 1) / kMxGroupKs;
   const int KS = a.KS;
+  const int KSG = (KS + tiles.ng - 1) / tiles.ng;  // K-steps per group
 
   if (warp == 0 || warp == 3) {
     // ===== source producers (one thread each in warps 0 and 3, on different SM
@@ -307,7 +316,8 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         const int j = tiles.at(i);
         if (j < 0) break;
         const int col = j * kMixTile;
-        for (int ks = 0; ks < KS; ++ks) {
+        const int kg0 = tiles.group(i) * KSG, kg1 = min(KS, kg0 + KSG);
+        for (int ks = kg0; ks < kg1; ++ks) {
           const int2 info = s_ksn[ks];
           const int n = info.y;  // multiple of 4
           const int skip = pos + n > RING ? RING - pos : 0;
@@ -341,7 +351,8 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       unsigned gph = 0;
       for (int i = 0;; ++i) {
         if (tiles.at(i) < 0) break;
-        for (int ks = 0; ks < KS; ++ks) {
+        const int kg0 = tiles.group(i) * KSG, kg1 = min(KS, kg0 + KSG);
+        for (int ks = kg0; ks < kg1; ++ks) {
           PROF_WAIT(0, mbar_wait_sleep(&g_empty[gs], gph ^ 1u));
           mbar_arrive_expect_tx(&g_full[gs], (unsigned)gbytes);
           bulk_load(sG + gs * gbytes, a.g + (long long)ks * gbytes, (unsigned)gbytes, &g_full[gs]);
@@ -364,7 +375,8 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         PROF_WAIT(2, mbar_wait_sleep(acc_empty, cph ^ 1u));  // the epilogue has drained the accumulators
         cph ^= 1u;
         tmem_fence_after();
-        for (int ks = 0; ks < KS; ++ks) {
+        const int kg0 = tiles.group(i) * KSG, kg1 = min(KS, kg0 + KSG);
+        for (int ks = kg0; ks < kg1; ++ks) {
           PROF_WAIT(0, mbar_wait_sleep(&g_full[gs], gph));
           PROF_WAIT(1, mbar_wait_sleep(&a_full[as], aph));
           tmem_fence_after();
@@ -373,7 +385,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           for (int rb = 0; rb < 2; ++rb) {
             const unsigned d = tbase + (unsigned)(rb * N);
             const unsigned ah = tbase + (unsigned)(kMxACol + 32 * as + 16 * rb), al = ah + 8;
-            mx_mma(d, ah, mx_sdesc(bh), idesc, ks > 0);
+            mx_mma(d, ah, mx_sdesc(bh), idesc, ks > kg0);
 #if TOEP_MIX_PRODUCTS > 1  // experiment knob: 3 products are needed for fp32 accuracy
             mx_mma(d, ah, mx_sdesc(bl), idesc, 1);
 #endif
@@ -405,6 +417,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
     int pos = 0, as = 0;
     unsigned aph = 0;
     const bool fixup = a.bad_list != nullptr;
+    float amax = 0.f;
 #if TOEP_MIX_PROF
     _tp = clock64();
 #endif
@@ -412,8 +425,10 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       const int j = tiles.at(i);
       if (j < 0) break;
       const int sexp = mx_tile_sexp(a, j);  // (samples past T arrive as zeros: TMA out-of-bounds fill)
-      float amax = 0.f;
-      for (int ks = 0; ks < KS; ++ks) {
+      const int grp = tiles.group(i);
+      if (grp == 0) amax = 0.f;
+      const int kg0 = grp * KSG, kg1 = min(KS, kg0 + KSG);
+      for (int ks = kg0; ks < kg1; ++ks) {
         const int n = s_ksn[ks].y;  // 16 rows x c slots (c = sources per row, one size class per K-step)
         const int4 ra = s_rows4[4 * ks + 2 * half], rbv = s_rows4[4 * ks + 2 * half + 1];  // this warp's 8 rows
         const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
@@ -477,7 +492,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         pos += n;
         ++seq;
       }
-      if (!a.bad_list) {  // tile max (unscaled) for the fixup scan
+      if (!a.bad_list && grp == tiles.ng - 1) {  // tile max (at the launch scale) for the fixup scan
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         if (lane == 0) s_bmax[bw] = amax;
@@ -550,6 +565,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       named_sync(2, 32 * kMxEpiWarps);
       // combine the 8 windows (fixed order): position P of the tile's 256 + K - 1
       const long long t0 = (long long)j * kMixTile;
+      const bool grp0 = tiles.group(i) == 0;
       const float2 inv = p2f2(-mx_tile_sexp(a, j));
       const int npos = kMixTile + K - 1;
       const int et = tid - 32 * (4 + kMxBuildWarps);
@@ -562,10 +578,16 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           if (P >= b && P < b + win) acc += eb[(w * ears + e) * win + (P - b)];
         }
         acc = acc * inv.x * inv.y;
+        // the first K-step group of a tile stores, later groups add (same
+        // thread, same position: program order)
         if (P < kMixTile) {
-          if (t0 + P < a.zlen) a.z[(long long)e * a.z_pitch + t0 + P] = acc;
+          if (t0 + P < a.zlen) {
+            float* zp = a.z + (long long)e * a.z_pitch + t0 + P;
+            *zp = grp0 ? acc : *zp + acc;
+          }
         } else {
-          a.ovh[((long long)j * ears + e) * a.ovh_pitch + (P - kMixTile)] = acc;
+          float* op = a.ovh + ((long long)j * ears + e) * a.ovh_pitch + (P - kMixTile);
+          *op = grp0 ? acc : *op + acc;
         }
       }
       named_sync(2, 32 * kMxEpiWarps);  // the windows are rewritten for the next tile

@@ -180,3 +180,16 @@ def test_mix_paths_shapes(mods, cuda, monkeypatch, mma):
                                      0, T + cfg.M - 1)
             for e in range(ears):
                 assert rel_l2(o2[e].double().cpu().numpy(), ref2[e]) <= TOL, ("sub", K, e)
+
+
+def test_mix_many_sources_kstep_groups(mods, cuda):
+    """6,000 sources over 1,250 directions: more than 96 K-steps per tile, so
+    the tensor mix accumulates a tile in groups (the first stores, the others
+    add) -- the accumulation error stays bounded whatever the source count."""
+    batch, synth, model_rows, _, _ = mods
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("g", ny=3_000, M=200, K=100, nnz=24, dirs=1250, ears=2, sources=6000)
+    ms = synth.models(cfg, seed=77)
+    sd = synth.source_directions(cfg.sources, cfg.dirs, seed=8)
+    y = synth.device_sources(cfg.sources, cfg.ny, seed=13)
+    _mix_check(mods, ms, sd, y, [(0, 1000), (1_400, 900), (cfg.ny - 700, 899)])

@@ -49,18 +49,27 @@ def check(S, T, nnz=24, dirs=1250, seed=5, scale=1.0, windows=None):
 
 if __name__ == "__main__":
     torch.cuda.set_device(0)
-    if "--prof" in sys.argv:  # one cfg5 partial with a TOEP_MIX_PROF build (TOEP_LIB=...)
+    if "--prof" in sys.argv:  # one cfg5 partial with a TOEP_MIX_PROF build (TOEP_LIB=...); --share R/N: rank R of N
+        from paper_1502_03162_b200 import dist as tdist
         cfg = synth.CONFIGS["cfg5"]
         ms = synth.models(cfg, seed=5)
         sd = synth.source_directions(cfg.sources, cfg.dirs, seed=5)
-        y = synth.device_sources(cfg.sources, cfg.ny, seed=1000)
+        if "--share" in sys.argv:
+            r, n = (int(v) for v in sys.argv[sys.argv.index("--share") + 1].split("/"))
+            mine = tdist.partition_by_direction(sd, n)[r]
+            sd = sd[mine]
+        y = synth.device_sources(sd.size, cfg.ny, seed=1000)
         mix = batch.MixRenderer(ms, sd, cfg.ny)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         z = mix.alloc_z()
         mix.partial(y, z=z)
         torch.cuda.synchronize()
         print("---- second call", flush=True)
+        ev[0].record()
         mix.partial(y, z=z)
+        ev[1].record()
         torch.cuda.synchronize()
+        print("partial ms %.3f (%d sources)" % (ev[0].elapsed_time(ev[1]), sd.size), flush=True)
         sys.exit(0)
     for S, T, sc in [(6, 3000, 1.0), (192, 100_000, 1.0), (300, 20_000, 1e-9), (300, 20_000, 1e9), (64, 1000, 1.0)]:
         p, e = check(S, T, scale=sc)

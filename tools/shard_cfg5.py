@@ -36,13 +36,14 @@ def main():
     for world in (1, args.world):
         parts = tdist.partition_by_direction(sd, world)
         for r, mine in enumerate(parts):
-            y = synth.device_sources(int(mine.size), cfg.ny, seed=1000 + r)
+            y = synth.device_sources_indexed(mine, cfg.ny, seed=1000)
             mix = batch.MixRenderer(ms, sd[mine], cfg.ny)
             z = mix.alloc_z()
-            ms_steps, _ = timed(lambda: mix.partial(y, z=z, check_finite=False), args.steps, 2, 1, flush)
+            # warm-up long enough for the board's power/clock state to settle on this share's load
+            ms_steps, _ = timed(lambda: mix.partial(y, z=z, check_finite=False), args.steps, 10, 1, flush)
             res["shares"].append({"world": world, "rank": r, "sources": int(mine.size),
                                   "directions": int(np.unique(sd[mine]).size),
-                                  "ms": statistics.mean(ms_steps)})
+                                  "ms": statistics.median(ms_steps)})
             del y, mix, z
             torch.cuda.empty_cache()
     one = [s["ms"] for s in res["shares"] if s["world"] == 1][0]

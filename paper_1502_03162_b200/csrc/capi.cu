@@ -247,6 +247,26 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pai
                         long long nx, float* out, long long out_pitch, cudaStream_t st, int* nonfinite = nullptr,
                         bool padded_out = false) {
   const long long out_len = nx + t->length - 1;
+  if (nrows == 1 && !nonfinite && nx <= (1LL << 20)) {
+    // one row of a per-call convolution: the banded kernel is one launch with
+    // exact-length writes (the TMEM-window kernel's persistent grid, TMEM
+    // allocation and 16-byte tail handling cost more than its speed wins at this size)
+    SparseGenericArgs g{};
+    g.x = x;
+    g.nx = nx;
+    g.x_pitch = 0;
+    g.rows_per_x = 1;
+    g.taps = t->d_raw + (size_t)row0 * t->tap_stride;
+    g.row_nnz = t->d_nnz + row0;
+    g.tap_stride = t->tap_stride;
+    g.rows = 1;
+    g.out = out;
+    g.out_len = out_len;
+    g.out_pitch = out_len;
+    cudaError_t e = launch_sparse_generic(g, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_sparse_generic");
+    return TOEP_OK;
+  }
   if (t->kwin > 0 && nrows == 1 && !padded_out && (out_len % 4 != 0 || !aligned16(out))) {
     // one row, exactly out_len samples: the kernel's stores move whole 16-byte
     // units, so it renders into a padded scratch row that is copied out exact
@@ -321,13 +341,15 @@ static int reflect_rows(const toep_taps* t, int row0, int nrows, const int4* pai
 }
 
 static int dense_fir(const float* x, long long nx, long long x_pitch, const float* h_pad, int nh_pad, int h_pitch,
-                     int channels, float* out, long long out_len, long long out_pitch, cudaStream_t st) {
+                     int channels, float* out, long long out_len, long long out_pitch, cudaStream_t st,
+                     int nh = -1) {
   FirArgs a{};
   a.x = x;
   a.nx = nx;
   a.x_pitch = x_pitch;
   a.h = h_pad;
   a.nh_pad = nh_pad;
+  a.nh = nh < 0 ? nh_pad : nh;
   a.h_pitch = h_pitch;
   a.out = out;
   a.out_len = out_len;
@@ -359,13 +381,8 @@ int toep_conv_dense(const float* y, int64_t ny, const float* taps, int64_t ntaps
   cudaStream_t st = S(stream);
   const long long nh_pad = round_up(ntaps, 16);
   if (nh_pad > (1LL << 30)) return fail(TOEP_ERR_UNSUPPORTED, "too many taps");
-  float* h = nullptr;
-  TOEP_CUDA(pool_alloc(&h, nh_pad * sizeof(float), st));
-  cudaError_t e = cudaMemsetAsync(h, 0, nh_pad * sizeof(float), st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h, taps, ntaps * sizeof(float), cudaMemcpyDeviceToDevice, st);
-  int rc = (e == cudaSuccess) ? dense_fir(y, ny, 0, h, (int)nh_pad, 0, 1, out, ny + ntaps - 1, 0, st)
-                              : cuda_fail(e, "toep_conv_dense staging");
-  cudaFreeAsync(h, st);
+  // one launch: the FIR kernel reads taps past ntaps as zeros
+  const int rc = dense_fir(y, ny, 0, taps, (int)nh_pad, 0, 1, out, ny + ntaps - 1, 0, st, (int)ntaps);
   if (rc == TOEP_OK && macs) *macs = (int64_t)ntaps * ny;  // _kernels.pyx:24
   return rc;
 }

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kThreads) k_fir(FirArgs a) {
   for (int j0 = 0; j0 < a.nh_pad; j0 += kFirChunk) {
     const int nch = min(kFirChunk, a.nh_pad - j0);
     __syncthreads();
-    for (int i = tid; i < nch; i += kThreads) s_h[i] = h[j0 + i];
+    for (int i = tid; i < nch; i += kThreads) s_h[i] = j0 + i < a.nh ? h[j0 + i] : 0.f;
     // s_x[k] = x[T0 - j0 - nch + k], k in [0, kW + nch)
     const long long xs = T0 - j0 - nch;
     for (int i = tid; i < kW + nch; i += kThreads) {

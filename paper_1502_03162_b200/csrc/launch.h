@@ -124,8 +124,9 @@ struct FirArgs {
   const float* x;
   long long nx;
   long long x_pitch;
-  const float* h;        // [channels][h_pitch] zero padded to a multiple of 16
-  int nh_pad;
+  const float* h;        // [channels][h_pitch]; taps past nh read as zero
+  int nh_pad;            // nh rounded up to 16 (the loop structure)
+  int nh;                // taps actually stored per channel
   int h_pitch;
   float* out;
   long long out_len;

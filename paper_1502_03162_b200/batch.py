@@ -161,10 +161,18 @@ class MixRenderer(_ModelSet):
         self.mixer = _lib.NativeMixer(self.native, self.src_dir, self.T)
         self.z_len = self.mixer.z_len()
         self.out_len = self.mixer.out_len()
-        #: "tensor" (tcgen05 GEMM over direction sums + overlap-add) or "window" (TMEM window + FFMA2)
-        self.path = self.mixer.path()
-        #: kernel launches per partial() call
-        self.kernels = self.mixer.kernels()
+
+    @property
+    def path(self) -> str:
+        """"tensor" (tcgen05 GEMM over direction sums + overlap-add) or "window"
+        (TMEM window + FFMA2); the tensor plan built at the first partial() may
+        fall back to "window" (tables beyond shared memory)."""
+        return self.mixer.path()
+
+    @property
+    def kernels(self) -> int:
+        """Kernel launches per partial() call."""
+        return self.mixer.kernels()
 
     def alloc_z(self):
         t = _lib.require_cuda()

@@ -92,8 +92,8 @@ def test_render_transient_next_to_silence(mods):
 def _mix_check(mods, ms, sd, y, windows):
     batch, synth, model_rows, _, _ = mods
     mix = batch.MixRenderer(ms, sd, y.shape[1])
-    assert mix.path == "tensor"
     out = mix.render(y)
+    assert mix.path == "tensor"
     T = y.shape[1]
     f = np.stack([m.resonance_taps for m in ms])
     yh = y.double().cpu().numpy()

@@ -68,6 +68,7 @@ def test_cfg5_full_size(mods, cuda):
     assert mix.path == "tensor"
     out = mix.render(y)
     torch.cuda.synchronize()
+    assert mix.path == "tensor"  # the plan fitted (no fallback)
     assert out.shape == (2, T + 199)
     assert bool(torch.isfinite(out).all())
     windows = [(0, 2048), (256 * 5625 - 100, 700), (2048 * 700 - 5, 1200), (1_000_003, 1500),

@@ -102,6 +102,10 @@ int toep_renderer_destroy(toep_renderer* r);
 int64_t toep_renderer_out_len(const toep_renderer* r, int64_t ny);
 /* Minimum row pitch (floats) accepted by toep_renderer_render. */
 int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny);
+/* Recommended row pitch (floats): out_len rounded up to 32 (128-byte rows,
+ * whole cache lines per store); any pitch >= min_pitch with pitch % 4 == 0
+ * is accepted. */
+int64_t toep_renderer_pitch(const toep_renderer* r, int64_t ny);
 /* Every (ear, direction): out[row*out_pitch + t] = ((y*f_ear)*g_row)[t],
  * t < out_len; samples in [out_len, min_pitch) of a row may be written
  * (with zeros).  out must be 16-byte aligned and out_pitch % 4 == 0.

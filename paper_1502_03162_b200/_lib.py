@@ -24,6 +24,7 @@ EXPORTS = (
     "toep_conv_dense", "toep_conv_sparse", "toep_fft", "toep_fft_spectrum", "toep_fft_conv",
     "toep_taps_create", "toep_taps_destroy", "toep_taps_info", "toep_taps_conv",
     "toep_renderer_create", "toep_renderer_destroy", "toep_renderer_out_len", "toep_renderer_min_pitch",
+    "toep_renderer_pitch",
     "toep_renderer_render", "toep_renderer_reflect", "toep_renderer_check", "toep_renderer_path",
     "toep_renderer_kernels",
     "toep_mixer_create", "toep_mixer_destroy", "toep_mixer_z_len", "toep_mixer_out_len",
@@ -77,6 +78,7 @@ def load_library(path: str = LIB_PATH):
         "toep_renderer_destroy": (ctypes.c_int, [_vp]),
         "toep_renderer_out_len": (_i64, [_vp, _i64]),
         "toep_renderer_min_pitch": (_i64, [_vp, _i64]),
+        "toep_renderer_pitch": (_i64, [_vp, _i64]),
         "toep_renderer_render": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
         "toep_renderer_reflect": (ctypes.c_int, [_vp, _i32, _vp, _i64, _vp, _i64, _vp]),
         "toep_renderer_check": (ctypes.c_int, [_vp, _i32p, _vp]),
@@ -225,6 +227,10 @@ class NativeRenderer:
 
     def min_pitch(self, ny: int) -> int:
         return int(load_library().toep_renderer_min_pitch(self._h, int(ny)))
+
+    def pitch(self, ny: int) -> int:
+        """Recommended row pitch (128-byte rows)."""
+        return int(load_library().toep_renderer_pitch(self._h, int(ny)))
 
     def render(self, y, out, pitch: int, stream=None):
         check(load_library().toep_renderer_render(self._h, dptr(y), int(y.numel()), dptr(out), int(pitch),

@@ -90,9 +90,9 @@ class BatchRenderer(_ModelSet):
         return ny + self.M - 1
 
     def alloc(self, ny: int):
-        """Output buffer [ears, dirs, pitch] (pitch >= out_len, 16-byte rows)."""
+        """Output buffer [ears, dirs, pitch] (pitch >= out_len, 128-byte rows)."""
         t = _lib.require_cuda()
-        pitch = self.native.min_pitch(ny)
+        pitch = self.native.pitch(ny)
         return t.empty((self.ears, self.dirs, pitch), device="cuda", dtype=t.float32)
 
     def render_all(self, y, out=None, stream=None, check_finite: bool = True):

@@ -587,6 +587,13 @@ int64_t toep_renderer_min_pitch(const toep_renderer* r, int64_t ny) {
   return r ? round_up(toep_renderer_out_len(r, ny), 4) : -1;
 }
 
+// rows on 128-byte boundaries: every TMA store box row then covers whole
+// cache lines (the tensor path's store stream is ~1.3x faster than at a
+// 16-byte-aligned pitch; tools/microbench/tma_store_rate.cu)
+int64_t toep_renderer_pitch(const toep_renderer* r, int64_t ny) {
+  return r ? round_up(toep_renderer_out_len(r, ny), 32) : -1;
+}
+
 // tensor-core path unless the taps are so sparse (<= 8 per row) that the FFMA
 // kernel already meets the write roofline while the GEMM pays for KPAD > 128
 // zero columns (cfg3 sweep)

@@ -67,6 +67,9 @@ def test_render_stays_in_bounds(mods, monkeypatch, K, nnz, path, env):
     # min_pitch (TMA / bulk stores move whole 16-byte units); nothing beyond
     mp = br.native.min_pitch(cfg.ny)
     assert mp == (L + 3) // 4 * 4
+    # the recommended pitch (BatchRenderer.alloc) keeps rows on 128-byte lines
+    assert br.native.pitch(cfg.ny) == (L + 31) // 32 * 32
+    assert br.alloc(cfg.ny).shape[2] == (L + 31) // 32 * 32
     tail = host[:, :, L:mp]
     assert (np.isnan(tail) | (tail == 0)).all(), "non-zero store past out_len"
     assert np.isnan(host[:, :, mp:]).all(), "store into row padding"

@@ -234,6 +234,31 @@ def _ref_render_rows(task):
     return n
 
 
+def _ref_worker_init_cfg3(payload):
+    """cfg3 workers: y*f of every (point, ear) rendered up front in the parent
+    (shared by fork) -- the reference renders it once per renderer and reuses
+    it for all 1,250 directions (< 3% of a point's work)."""
+    _ref_worker_init(payload)
+    _REF_STATE["yf"] = dict(payload["yf"])
+
+
+def _ref_render_point_rows(task):
+    """cfg3 sweep: the Renderer.render composition for rows of one sweep point."""
+    p, ear, rows = task
+    st = _REF_STATE
+    mod = st["mod"]
+    pt = st["pts"][p]
+    if (p, ear) not in st["yf"]:
+        st["yf"][(p, ear)] = mod.conv_dense(st["y"], pt["f"][ear])[0]
+    yf = st["yf"][(p, ear)]
+    n = 0
+    for r in rows:
+        idx, vals = pt["rows"][r]
+        out, _ = mod.conv_sparse(yf, idx, vals, pt["K"])
+        n += out.size
+    return n
+
+
 def _ref_mix_sources(task):
     """Per-source Renderer.render for both ears, accumulated in fp64 (mixdown configs)."""
     st = _REF_STATE
@@ -290,6 +315,55 @@ def reference_step_factory(workload: str, cores: int):
 
         desc = "full %s per step: %d channels x %d samples, Renderer.render composition" % (
             workload, cfg.ears * cfg.dirs, cfg.ny + cfg.M - 1)
+        kind = "reference" if _probe_ref() else "port"
+        return step, desc, kind, pool, single
+    if workload == "cfg3":
+        # every sweep point, bounded: 4 x cores directions of each ear over the
+        # full 441,000-sample source (the reference's per-row cost does not
+        # depend on which directions); per-point rates kept on step.rates
+        pts = synth.cfg3_points()
+        y = synth.source(pts[0].ny, seed=3)
+        payload = {"y": y, "pts": []}
+        for cfg in pts:
+            ms = synth.models(cfg, seed=cfg.K * 1000 + cfg.nnz)
+            payload["pts"].append({"f": [m.resonance_taps for m in ms], "rows": model_rows(ms), "K": cfg.K})
+        import oracle
+        mod = oracle.ref_kernels() or oracle
+        payload["yf"] = {(p, e): mod.conv_dense(y, f)[0] for p, pt in enumerate(payload["pts"])
+                         for e, f in enumerate(pt["f"])}
+        ctx = mp.get_context("fork")
+        pool = ctx.Pool(cores, initializer=_ref_worker_init_cfg3, initargs=(payload,))
+        nd = min(pts[0].dirs, max(8, 4 * cores))
+        tasks = [[(p, e, list(range(e * cfg.dirs + d, e * cfg.dirs + min(nd, d + 4))))
+                  for e in range(cfg.ears) for d in range(0, nd, 4)] for p, cfg in enumerate(pts)]
+
+        def step():
+            n = 0
+            for p, cfg in enumerate(pts):
+                t0 = time.perf_counter()
+                k = sum(pool.map(_ref_render_point_rows, tasks[p], chunksize=1))
+                dt = time.perf_counter() - t0
+                r = step.rates.setdefault(cfg.name, [0, 0.0])
+                r[0] += k
+                r[1] += dt
+                n += k
+            return n
+        step.rates = {}
+
+        def single(budget_s=3.0):
+            # one core: the nnz-16 point at K 100 (cfg2's sparsity), its y*f precomputed
+            p = [c.name for c in pts].index("cfg3_K100_nnz16")
+            _ref_worker_init_cfg3(payload)
+            n, i = 0, 0
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < budget_s and i < len(tasks[p]):
+                n += _ref_render_point_rows(tasks[p][i])
+                i += 1
+            return n / (time.perf_counter() - t0)
+
+        desc = ("17 cfg3 points per step, each %d directions x 2 ears x %d samples (full source), "
+                "Renderer.render composition (y*f per ear rendered once, before timing)"
+                % (nd, pts[0].ny + pts[0].M - 1))
         kind = "reference" if _probe_ref() else "port"
         return step, desc, kind, pool, single
     if workload in ("cfg4", "cfg5"):
@@ -401,7 +475,7 @@ def _cpu_model() -> str:
 def _ref_factory(wl, cores):
     if wl == "cfg4":
         return reference_stream_factory(cores)
-    return reference_step_factory("cfg2" if wl == "cfg3" else wl, cores)
+    return reference_step_factory(wl, cores)
 
 
 METRIC = "output samples/s (src x dir x ear)"
@@ -460,6 +534,8 @@ def run_reference(args, world, rank):
                          "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if getattr(step, "rates", None):
+        line["cpu_baseline"]["points"] = {k: n / t for k, (n, t) in step.rates.items()}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -481,9 +557,12 @@ def cpu_baseline_line(workload):
     finally:
         pool.close()
         pool.join()
-    return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": kind,
-            "sample": "%s; %d repetitions" % (desc, reps), "seconds": dt,
-            "single_core_value": single(3.0), "cpu_model": _cpu_model()}
+    out = {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": kind,
+           "sample": "%s; %d repetitions" % (desc, reps), "seconds": dt,
+           "single_core_value": single(3.0), "cpu_model": _cpu_model()}
+    if getattr(step, "rates", None):
+        out["points"] = {k: m / t for k, (m, t) in step.rates.items()}
+    return out
 
 
 # ------------------------------------------------------------ our arm ------
@@ -923,6 +1002,11 @@ def main():
         line["gpu_launches"] += fr["gpu_launches"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_line(args.workload)
+        for pt in line.get("points", ()):  # cfg3: the reference beside every point
+            cpu = line["cpu_baseline"].get("points", {}).get(pt["point"])
+            if cpu:
+                pt["cpu_samples_per_s"] = cpu
+                pt["vs_cpu"] = pt["samples_per_s"] / cpu
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -34,6 +34,9 @@ timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_m
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_render_mma -s 4 -c 2 \
   -o "$O/render_mma_full" -f python bench.py --workload cfg2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
   > /dev/null 2>&1
+timeout 900 ncu --profile-from-start off --clock-control none --csv \
+  --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  --log-file "$O/cfg3_points.csv" python tools/cfg3_points_ncu.py run > "$O/cfg3_points.jsonl" 2> /dev/null
 echo "ncu done"
 
 # back in the container:
@@ -41,4 +44,5 @@ echo "ncu done"
 #   python tools/ncu_summary.py --launches gpurun_out/$R/launches_cfg5.csv > profiles/${R}_cfg5_launches.txt
 #   python tools/ncu_summary.py gpurun_out/$R/mix_mma_full.ncu-rep > profiles/${R}_cfg5_k_mix_mma_full.txt
 #   python tools/ncu_summary.py gpurun_out/$R/render_mma_full.ncu-rep > profiles/${R}_cfg2_k_render_mma_full.txt
+#   python tools/cfg3_points_ncu.py summarize gpurun_out/$R/cfg3_points.csv gpurun_out/$R/cfg3_points.jsonl > profiles/${R}_cfg3_points_ncu.txt
 #   update profiles/traffic.json (dram bytes of one mix / one render launch) from those summaries

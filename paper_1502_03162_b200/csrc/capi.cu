@@ -835,11 +835,13 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   for (int i = 0; i < count; ++i) ord[i] = i;
   std::stable_sort(ord.begin(), ord.end(), [dir](int x, int y2) { return dir[x] < dir[y2]; });
   // rows: a direction's sources in groups of kMixRowSrcs, the remainder in one
-  // smaller row; K-steps hold 16 rows of ONE size class c (4, 3, 2, 1 sources),
-  // so a K-step is 16c consecutive ring slots, row r at slots [c r, c r + c)
-  // (the builders' loads use compile-time offsets, no per-row predicates);
-  // only the last K-step of a class has padding rows (out-of-range source
-  // rows: TMA fills their slots with zeros, no memory traffic)
+  // smaller row.  Half K-steps hold 8 rows of ONE size class c (4, 3, 2, 1
+  // sources), so a half is 8c consecutive ring slots, row r at [c r, c r + c)
+  // (each builder warp takes one half: compile-time load offsets, no per-row
+  // predicates); a K-step pairs two halves, classes c0 and c1, ks.y = n | c0 << 16
+  // with n = 8 (c0 + c1) slots.  Only a class's last half has padding rows
+  // (out-of-range source rows: TMA fills their slots with zeros, no memory
+  // traffic), plus one padding half of class 1 when the count of halves is odd.
   struct Row { int d, first, cnt; };
   std::vector<Row> byc[kMixRowSrcs + 1];
   for (int p = 0; p < count;) {
@@ -851,22 +853,75 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
     }
     p = q;
   }
+  // Rebalance the classes: splitting the e = (rows mod 8) rows of a class's
+  // last, partly padded half into two smaller rows each (c = a + (c - a))
+  // removes that half; keep a split when the modelled cost -- 40 slot loads
+  // per K-step (MMAs, G stage, per-step builder work) + 1 per slot, padding
+  // included -- drops.  Every source stays in exactly one row.
+  {
+    auto cost = [](const size_t* nr) {
+      size_t halves = 0, slots = 0;
+      for (int c = 1; c <= kMixRowSrcs; ++c) {
+        halves += (nr[c] + 7) / 8;
+        slots += (nr[c] + 7) / 8 * 8 * c;
+      }
+      if (halves & 1) slots += 8;
+      return 40 * ((halves + 1) / 2) + slots;
+    };
+    for (;;) {
+      size_t nr[kMixRowSrcs + 1];
+      for (int c = 0; c <= kMixRowSrcs; ++c) nr[c] = byc[c].size();
+      const size_t base = cost(nr);
+      size_t best = base;
+      int bc = 0, ba = 0;
+      for (int c = 2; c <= kMixRowSrcs; ++c)
+        for (int a = 1; 2 * a <= c; ++a) {
+          const size_t e = nr[c] % 8;
+          if (!e) continue;
+          size_t t[kMixRowSrcs + 1];
+          std::copy(nr, nr + kMixRowSrcs + 1, t);
+          t[c] -= e;
+          t[a] += e;
+          t[c - a] += e;
+          const size_t v = cost(t);
+          if (v < best) {
+            best = v;
+            bc = c;
+            ba = a;
+          }
+        }
+      if (!bc) break;
+      for (size_t e = byc[bc].size() % 8; e > 0; --e) {
+        const Row w = byc[bc].back();
+        byc[bc].pop_back();
+        byc[ba].push_back({w.d, w.first, ba});
+        byc[bc - ba].push_back({w.d, w.first + ba, bc - ba});
+      }
+    }
+  }
+  struct Half { int c; const Row* rows; int nr; };  // nr <= 8 real rows
+  std::vector<Half> halves;
+  for (int c = kMixRowSrcs; c >= 1; --c)
+    for (size_t i = 0; i < byc[c].size(); i += 8)
+      halves.push_back({c, byc[c].data() + i, (int)std::min<size_t>(8, byc[c].size() - i)});
+  if (halves.size() & 1) halves.push_back({1, nullptr, 0});
   std::vector<int2> ks;
   std::vector<int> rinfo;    // [KS][16] (gamma_d + 128) << 9 (the fixup pass scales per row)
   std::vector<float> rowf;   // [KS][16] main-pass multipliers 2^(sexp - gamma_d)
   bool clamped = false;
   std::vector<int> ks_dirs;  // [KS][16] direction per row (-1 empty), gamma_d
-  std::vector<unsigned short> src;  // K-step source lists: 16 rows x c entries
-  for (int c = kMixRowSrcs; c >= 1; --c) {
-    const std::vector<Row>& rows = byc[c];
-    for (size_t i = 0; i < rows.size(); i += 16) {
-      const int nr = (int)std::min<size_t>(16, rows.size() - i);
-      ks.push_back(make_int2((int)src.size(), 16 * c));
-      for (int k = 0; k < 16; ++k)
-        for (int u = 0; u < c; ++u) src.push_back((unsigned short)(k < nr ? ord[rows[i + k].first + u] : count));
-      for (int k = 0; k < 16; ++k) {
-        if (k < nr) {
-          const Row& w = rows[i + k];
+  std::vector<unsigned short> src;  // K-step source lists: 8 rows x c0, then 8 rows x c1
+  for (size_t hk = 0; hk < halves.size(); hk += 2) {
+    const Half& h0 = halves[hk];
+    const Half& h1 = halves[hk + 1];
+    ks.push_back(make_int2((int)src.size(), (8 * (h0.c + h1.c)) | (h0.c << 16)));
+    for (const Half* h : {&h0, &h1})
+      for (int k = 0; k < 8; ++k)
+        for (int u = 0; u < h->c; ++u) src.push_back((unsigned short)(k < h->nr ? ord[h->rows[k].first + u] : count));
+    for (const Half* h : {&h0, &h1}) {
+      for (int k = 0; k < 8; ++k) {
+        if (k < h->nr) {
+          const Row& w = h->rows[k];
           float mx = 0.f;
           for (int e = 0; e < r->ears; ++e) {
             const int row = e * r->dirs + w.d;

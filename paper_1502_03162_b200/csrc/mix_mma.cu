@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         const int kg0 = tiles.group(i) * KSG, kg1 = min(KS, kg0 + KSG);
         for (int ks = kg0; ks < kg1; ++ks) {
           const int2 info = s_ksn[ks];
-          const int n = info.y;  // multiple of 4
+          const int n = info.y & 0xffff;  // slots, a multiple of 8
           const int skip = pos + n > RING ? RING - pos : 0;
           while (seq - fseq >= kMxKR || held + skip + n > RING) {
             PROF_WAIT(0, mbar_wait_sleep(&src_empty[fseq % kMxKR], (unsigned)((fseq / kMxKR) & 1)));
@@ -429,7 +429,8 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       if (grp == 0) amax = 0.f;
       const int kg0 = grp * KSG, kg1 = min(KS, kg0 + KSG);
       for (int ks = kg0; ks < kg1; ++ks) {
-        const int n = s_ksn[ks].y;  // 16 rows x c slots (c = sources per row, one size class per K-step)
+        const int ksy = s_ksn[ks].y;  // n | c0 << 16: 8 rows x c0 slots, then 8 rows x c1 (c = sources per row)
+        const int n = ksy & 0xffff, c0 = ksy >> 16;
         const int4 ra = s_rows4[4 * ks + 2 * half], rbv = s_rows4[4 * ks + 2 * half + 1];  // this warp's 8 rows
         const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
         if (pos + n > RING) pos = 0;
@@ -438,8 +439,8 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         PROF_MARK(7);
         float v[8];
         {
-          const int c = n >> 4;
-          const float* base = ring + (pos + 8 * c * half) * kMixTile + tt;  // this warp's first row
+          const int c = half ? (n >> 3) - c0 : c0;  // this warp's half: one size class
+          const float* base = ring + (pos + 8 * c0 * half) * kMixTile + tt;  // this warp's first row
           switch (c) {
             case 4: mx_row_sums<4>(base, v); break;
             case 3: mx_row_sums<3>(base, v); break;

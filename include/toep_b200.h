@@ -163,8 +163,8 @@ int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s
  * ears x round_up(length, 8) <= 208) or TOEP_PATH_WINDOW (TMEM window + FFMA2
  * per tap; TOEP_MIX_MMA=0 in the environment forces it). */
 int toep_mixer_path(const toep_mixer* m);
-/* Kernel launches per toep_mixer_partial call (tensor path: main pass, tile
- * scan, fixup pass for tiles outside the fp16-safe range, overhang carry). */
+/* Kernel launches per toep_mixer_partial call (tensor path: main pass, fixup
+ * pass for tiles outside the fp16-safe range, overhang carry + z check). */
 int toep_mixer_kernels(const toep_mixer* m);
 /* out[e] = f_e * z[e] (length out_len). */
 int toep_mixer_finish(const toep_mixer* m, const float* z, int64_t z_pitch, float* out, int64_t out_pitch,

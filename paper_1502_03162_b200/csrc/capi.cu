@@ -781,7 +781,7 @@ struct toep_mixer {
   unsigned char* d_mg = nullptr;
   float* d_ovh = nullptr;
   float* d_tmax = nullptr;
-  int* d_bad = nullptr;  // [n_tiles] list + count
+  int* d_bad = nullptr;  // [n_tiles] list + count + main-pass arrival counter
   std::vector<int2> h_taps;  // [rows][tap_stride] {offset, value bits}
   std::vector<int> h_nnz;
   const float* map_y = nullptr;  // source tensor map of the last call
@@ -994,7 +994,8 @@ static int mma_plan(toep_mixer* m, int s0, int count, cudaStream_t st) {
   if (e == cudaSuccess) e = cudaMalloc(&m->d_mg, G.size());
   if (e == cudaSuccess) e = cudaMalloc(&m->d_ovh, (size_t)m->n_tiles * r->ears * m->ovh_pitch * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_tmax, (size_t)m->n_tiles * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&m->d_bad, (size_t)(m->n_tiles + 1) * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_bad, (size_t)(m->n_tiles + 2) * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->d_bad + m->n_tiles, 0, 2 * sizeof(int), st);  // count, arrivals
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(m->d_msrc, src.data(), src.size() * sizeof(unsigned short), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(m->d_mks, ks.data(), KS * sizeof(int2), cudaMemcpyHostToDevice, st);
@@ -1084,7 +1085,9 @@ int toep_mixer_destroy(toep_mixer* m) {
 
 int64_t toep_mixer_z_len(const toep_mixer* m) { return m ? m->zlen : -1; }
 int toep_mixer_path(const toep_mixer* m) { return m ? (m->mma ? TOEP_PATH_TENSOR : TOEP_PATH_WINDOW) : -1; }
-int toep_mixer_kernels(const toep_mixer* m) { return m ? (m->mma ? 5 : 3) : -1; }
+// tensor path: main pass (its last CTA lists the fixup tiles), fixup pass,
+// finish (overhang carry + z check); window path: mix, reduce, carry
+int toep_mixer_kernels(const toep_mixer* m) { return m ? 3 : -1; }
 int64_t toep_mixer_out_len(const toep_mixer* m) { return m ? m->zlen + m->r->lf - 1 : -1; }
 
 int toep_mixer_partial(toep_mixer* m, const float* y, int64_t y_pitch, int32_t s0, int32_t count, float* z,

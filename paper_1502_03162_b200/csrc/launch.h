@@ -221,8 +221,13 @@ struct MixMmaArgs {
   const int* bad_list;   // fixup pass: tiles to re-render (null: every tile)
   const int* bad_count;
   int* nonfinite;
+  int* scan_list;        // main pass: where the last CTA lists the fixup tiles (null: no scan)
+  int* scan_count;
+  unsigned* scan_done;   // CTA arrival counter (zero between calls)
 };
-// main pass, bad-tile scan, fixup pass, overhang carry, z finite check (5 launches; 4 without the check)
+// main pass (its last CTA lists the tiles for the fixup pass), fixup pass,
+// finish (overhang carry + z finite check): 3 launches; bad_count[1] is the
+// main pass's arrival counter and must be zero before the first call
 // tm: 2-D tensor map over the sources {T, rows}, box {kMixTile, 1} (tile::gather4 loads)
 cudaError_t launch_mix_mma(const MixMmaArgs& a, const CUtensorMap& tm, int* bad_list, int* bad_count, int sm_count,
                            cudaStream_t st);

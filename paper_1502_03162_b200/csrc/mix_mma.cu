@@ -19,14 +19,14 @@
 // source sample from HBM (4 B per source sample, 47 GB at config 5).  The
 // W formulation needs no halo on the loads: a tile of 256 samples reads
 // exactly samples [t0, t0+256) of each source; the (K-1)-sample tail of its
-// overlap-add ("overhang") is kept per tile and added by k_mix_carry.
+// overlap-add ("overhang") is kept per tile and added by k_mix_finish.
 //
 // fp32 accuracy from fp16 operands as in render_mma.cu: x = hi + lo,
 // products hi*hi + hi*lo + lo*hi into fp32 TMEM accumulators.  G columns are
 // normalised per direction by 2^gamma_d (host); the A value of row d is
 // Y_d * 2^-gamma_d * 2^sexp (exact power-of-two scaling, undone in the
 // epilogue).  The launch scale 2^sexp is fixed per mixer; every tile records
-// max |Y_d 2^-gamma_d| and k_mix_scan lists the tiles whose values left the
+// max |Y_d 2^-gamma_d| and the main pass's last CTA lists the tiles whose values left the
 // fp16-safe window (overflow, or so small that the low half loses bits while
 // the tile still matters); a second launch of this kernel re-renders exactly
 // those tiles with their own scale.  Results are a deterministic function of
@@ -185,6 +185,13 @@ __device__ __forceinline__ int mx_tile_sexp(const MixMmaArgs& a, int j) {
   if (!a.bad_list) return a.sexp;
   const float m = a.tile_max[j];
   return m > 0.f ? a.sexp + 13 - ilogbf(m) : a.sexp;
+}
+// tiles the fixup pass re-renders: max |A| at the launch scale outside the
+// fp16-safe window [2^-3, 2^15] -- the hi half would overflow, or the lo half
+// of the tile's largest values would not be a normal fp16 number; all-zero
+// tiles are exact at any scale; non-finite input is reported by the z check
+__device__ __forceinline__ bool mx_tile_bad(float s) {
+  return isfinite(s) && s != 0.f && (s > 32768.f || s < 0.125f);
 }
 // 2^e for any e: two exact factors (each clamped to the normal range, where
 // the value they scale would under/overflow anyway)
@@ -502,6 +509,7 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
           float m = 0.f;
           for (int w = 0; w < kMxBuildWarps; ++w) m = fmaxf(m, s_bmax[w]);
           a.tile_max[j] = m;
+          __threadfence();  // before this CTA's arrival at the end (the last CTA scans the maxima)
         }
         named_sync(1, 32 * kMxBuildWarps);
       }
@@ -603,56 +611,59 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
   tmem_fence_before();
   __syncthreads();
   if (warp == 3) tmem_dealloc<512>(tbase);
-}
-
-// bad-tile list for the fixup pass (one CTA): tiles whose max |A| at the
-// launch scale left the fp16-safe window [2^-3, 2^15] -- the hi half would
-// overflow, or the lo half of the tile's largest values would not be a
-// normal fp16 number; all-zero tiles are exact at any scale
-__global__ void __launch_bounds__(1024) k_mix_scan(const float* __restrict__ tile_max, int n_tiles,
-                                                    int* __restrict__ list, int* __restrict__ count) {
-  if (threadIdx.x == 0) *count = 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < n_tiles; j += blockDim.x) {
-    const float s = tile_max[j];
-    if (!isfinite(s) || s == 0.f) continue;  // non-finite input: reported by the z check, not re-rendered
-    if (s > 32768.f || s < 0.125f) list[atomicAdd(count, 1)] = j;
+  if (a.scan_count) {  // main pass: the last CTA to finish lists the fixup pass's tiles
+    __shared__ int s_last, s_n;
+    if (tid == 0) {
+      __threadfence();  // this CTA's tile maxima before its arrival
+      s_last = atomicAdd(a.scan_done, 1u) == gridDim.x - 1;
+      s_n = 0;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int j = tid; j < a.n_tiles; j += kMxThreads)
+        if (mx_tile_bad(a.tile_max[j])) a.scan_list[atomicAdd(&s_n, 1)] = j;
+      __syncthreads();
+      if (tid == 0) {
+        *a.scan_count = s_n;
+        *a.scan_done = 0u;  // ready for the next call
+      }
+    }
   }
 }
 
-// z[e][256 (j+1) + p] += ovh[j][e][p]  (the last tile's overhang is stored)
-__global__ void k_mix_carry(float* __restrict__ z, long long z_pitch, long long zlen, const float* __restrict__ ovh,
-                            int ovh_pitch, int n_tiles, int ears, int nov) {
-  const long long total = (long long)n_tiles * ears * nov;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int p = (int)(i % nov);
-    const long long je = i / nov;
-    const int e = (int)(je % ears);
-    const long long j = je / ears;
-    const long long pos = (j + 1) * kMixTile + p;
-    if (pos >= zlen) continue;
-    const float v = ovh[(j * ears + e) * ovh_pitch + p];
-    float* zp = z + (long long)e * z_pitch + pos;
-    *zp = (j + 1 < n_tiles ? *zp : 0.f) + v;
-  }
-}
-
+// Finish of the partial, one pass over z: the per-tile overhangs (the K - 1
+// samples past each tile's end) are added at the next tile's start,
+// z[e][256 (j+1) + p] += ovh[j][e][p] (the last tile's overhang is stored),
+// and -- when `nonfinite` is set -- every finished sample is checked: the
 // fused input check of the tensor mixdown (the reference's DataError for
-// non-finite samples, engine/__init__.py:162-165): a non-finite source sample
+// non-finite samples, engine/__init__.py:162-165).  A non-finite source sample
 // makes its tile's z non-finite (sums, fp16 halves and products propagate
 // inf/NaN), so the finished z is checked instead of every source sample
-// (23 MB instead of 47 GB at config 5)
-__global__ void k_mix_zcheck(const float* __restrict__ z, long long z_pitch, long long zlen, int ears,
-                             int* __restrict__ nonfinite) {
+// (23 MB instead of 47 GB at config 5).
+__global__ void __launch_bounds__(256) k_mix_finish(float* __restrict__ z, long long z_pitch, long long zlen,
+                                                    const float* __restrict__ ovh, int ovh_pitch, int n_tiles,
+                                                    int ears, int nov, int* __restrict__ nonfinite) {
   bool bad = false;
   for (int e = 0; e < ears; ++e) {
-    const float* ze = z + (long long)e * z_pitch;
+    float* ze = z + (long long)e * z_pitch;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < zlen;
-         t += (long long)gridDim.x * blockDim.x)
-      bad |= !isfinite(ze[t]);
+         t += (long long)gridDim.x * blockDim.x) {
+      const long long j = t / kMixTile - 1;  // the tile whose overhang reaches t
+      const int p = (int)(t - (j + 1) * kMixTile);
+      float v;
+      if (j >= 0 && p < nov && j < n_tiles) {
+        const float o = ovh[(j * ears + e) * ovh_pitch + p];
+        v = (j + 1 < n_tiles ? ze[t] : 0.f) + o;
+        ze[t] = v;
+      } else {
+        if (!nonfinite) continue;
+        v = ze[t];
+      }
+      bad |= !isfinite(v);
+    }
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
 
 int mix_mma_nr(int K) { return (32 + K - 1 + 31) / 32; }
@@ -682,6 +693,9 @@ cudaError_t launch_mix_mma(const MixMmaArgs& a_in, const CUtensorMap& tm, int* b
   MixMmaArgs a = a_in;
   a.bad_list = nullptr;
   a.bad_count = nullptr;
+  a.scan_list = bad_list;  // the main pass's last CTA writes the fixup list
+  a.scan_count = bad_count;
+  a.scan_done = reinterpret_cast<unsigned*>(bad_count + 1);
   const int grid = std::max(1, std::min(sm_count, a.n_tiles));
   auto go = [&](const MixMmaArgs& x) -> cudaError_t {
     if (ch <= 7 && nr <= 5) return launch_mix_mma_t<7, 5>(x, tm, grid, st);
@@ -690,24 +704,18 @@ cudaError_t launch_mix_mma(const MixMmaArgs& a_in, const CUtensorMap& tm, int* b
   };
   cudaError_t e = go(a);
   if (e != cudaSuccess) return e;
-  k_mix_scan<<<1, 1024, 0, st>>>(a.tile_max, a.n_tiles, bad_list, bad_count);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   MixMmaArgs f = a;
   f.bad_list = bad_list;
   f.bad_count = bad_count;
+  f.scan_list = nullptr;
+  f.scan_count = nullptr;
   e = go(f);
   if (e != cudaSuccess) return e;
   const int nov = a.K - 1;
-  if (nov > 0) {
-    const long long total = (long long)a.n_tiles * a.ears * nov;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sm_count * 8);
-    k_mix_carry<<<std::max(blocks, 1), 256, 0, st>>>(a.z, a.z_pitch, a.zlen, a.ovh, a.ovh_pitch, a.n_tiles, a.ears,
-                                                      nov);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  if (a.nonfinite) {
+  if (nov > 0 || a.nonfinite) {
     const int blocks = (int)std::min<long long>((a.zlen + 255) / 256, (long long)sm_count * 8);
-    k_mix_zcheck<<<std::max(blocks, 1), 256, 0, st>>>(a.z, a.z_pitch, a.zlen, a.ears, a.nonfinite);
+    k_mix_finish<<<std::max(blocks, 1), 256, 0, st>>>(a.z, a.z_pitch, a.zlen, a.ovh, a.ovh_pitch, a.n_tiles, a.ears,
+                                                       nov, a.nonfinite);
     e = cudaGetLastError();
   }
   return e;

@@ -1270,9 +1270,9 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
   s->H = (int)round_up(std::max(1, r->g->length - 1), 4);
   s->zh = r->lf_pad;
   // 4 sources per CTA: ~1 CTA per SM for 512 sources, short per-thread tap chains
-  s->spc = std::max(1, std::min(4, (96 * 1024 / 4) / (s->H + block + 2 * r->ears * r->g->tap_stride + r->ears)));
+  s->spc = std::max(1, std::min(4, (96 * 1024 / 4) / (s->H + block + 2 * r->ears * ((r->g->tap_stride + 7) / 8 * 8) + r->ears)));
   s->ctas = (n_src + s->spc - 1) / s->spc;
-  const int groups = (s->ctas + 15) / 16;
+  const int groups = (s->ctas + kStreamGroup - 1) / kStreamGroup;
   cudaError_t e = cudaMalloc(&s->d_dir, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(s->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&s->d_yhist, (size_t)n_src * s->H * sizeof(float));
@@ -1315,8 +1315,8 @@ int toep_streamer_reset(toep_streamer* s, void* stream) {
   if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
   cudaStream_t st = S(stream);
   TOEP_CUDA(cudaMemsetAsync(s->d_yhist, 0, (size_t)s->S * s->H * sizeof(float), st));
-  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)((s->ctas + 15) / 16) * s->r->ears * s->zh * sizeof(float), st));
-  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, ((s->ctas + 15) / 16 + 1) * sizeof(unsigned int), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)((s->ctas + kStreamGroup - 1) / kStreamGroup) * s->r->ears * s->zh * sizeof(float), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, ((s->ctas + kStreamGroup - 1) / kStreamGroup + 1) * sizeof(unsigned int), st));
   return TOEP_OK;
 }
 

@@ -482,7 +482,8 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
 // sources' history.  Partials are reduced deterministically in two ticketed
 // levels (groups of kStreamGroup CTAs, then the groups), and the very last CTA
 // applies f_e over [z history | z block] and rolls the z history.
-constexpr int kStreamGroup = 16;
+// shared-memory tap-row pitch of k_stream_step (rows read 8 taps at a time)
+__host__ __device__ inline int stream_tap_pitch(int tap_stride) { return (tap_stride + 7) / 8 * 8; }
 
 
 __device__ __forceinline__ bool stream_last_arrival(unsigned int* ticket, unsigned int n) {
@@ -495,15 +496,35 @@ __device__ __forceinline__ bool stream_last_arrival(unsigned int* ticket, unsign
   return s_last;
 }
 
+#ifndef TOEP_STREAM_PROF
+#define TOEP_STREAM_PROF 0
+#endif
+#if TOEP_STREAM_PROF
+__device__ unsigned long long g_sprof[8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPROF(i) \
+  if (threadIdx.x == 0) atomicMax(&g_sprof[i], gtime())
+#else
+#define SPROF(i)
+#endif
+
 __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
   extern __shared__ __align__(16) float sm[];
+#if TOEP_STREAM_PROF
+  if (threadIdx.x == 0) atomicMin(&g_sprof[0], gtime());
+#endif
   const int tid = threadIdx.x;
   const int L = a.H + a.B;  // multiple of 4 (host checks)
   const int s0 = blockIdx.x * a.src_per_cta;
   const int ns = min(a.S - s0, a.src_per_cta);
+  const int tsp = stream_tap_pitch(a.tap_stride);
   float* s_w = sm;                                                // [ns][L]
-  int2* s_tap = reinterpret_cast<int2*>(sm + a.src_per_cta * L);  // [ns][ears][tap_stride]
-  int* s_nnz = reinterpret_cast<int*>(s_tap + a.src_per_cta * a.ears * a.tap_stride);
+  int2* s_tap = reinterpret_cast<int2*>(sm + a.src_per_cta * L);  // [ns][ears][tsp] (zero-padded rows)
+  int* s_nnz = reinterpret_cast<int*>(s_tap + a.src_per_cta * a.ears * tsp);
   float chk = 0.f;  // fused DataError check on the new block's samples
   {
     const int q4 = L / 4, h4 = a.H / 4;
@@ -518,31 +539,62 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
       }
       *reinterpret_cast<float4*>(&s_w[s * L + 4 * q]) = v;
     }
-    // this CTA's sources' tap rows are contiguous in the per-source table
+    // this CTA's sources' tap rows are contiguous in the per-source table;
+    // shared rows padded to tsp (a multiple of 8) with zero taps
     const int2* st = a.src_taps + (long long)s0 * a.ears * a.tap_stride;
-    for (int i = tid; i < ns * a.ears * a.tap_stride; i += blockDim.x) s_tap[i] = __ldg(st + i);
+    for (int i = tid; i < ns * a.ears * tsp; i += blockDim.x) {
+      const int row = i / tsp, k = i - row * tsp;
+      s_tap[i] = k < a.tap_stride ? __ldg(st + (long long)row * a.tap_stride + k) : make_int2(0, 0);
+    }
     for (int i = tid; i < ns * a.ears; i += blockDim.x) s_nnz[i] = __ldg(a.src_nnz + (long long)s0 * a.ears + i);
   }
   __syncthreads();
+  SPROF(1);
   const int t = tid;
   float acc0 = 0.f, acc1 = 0.f;
   if (t < a.B) {
+    // taps 8 at a time: the 8 (offset, value) pairs by four broadcast 16-byte
+    // loads, then 8 independent window loads (no load waits on another), two
+    // accumulators per ear (even / odd taps)
+    float acc0b = 0.f, acc1b = 0.f;
     for (int s = 0; s < ns; ++s) {
       const float* w = s_w + s * L + a.H + t;
-      const int2* t0 = s_tap + (s * a.ears) * a.tap_stride;
-      const int n0 = s_nnz[s * a.ears];
-#pragma unroll 4
-      for (int k = 0; k < n0; ++k) acc0 = fmaf(__int_as_float(t0[k].y), w[-t0[k].x], acc0);
-      if (a.ears > 1) {
-        const int2* t1 = t0 + a.tap_stride;
-        const int n1 = s_nnz[s * a.ears + 1];
-#pragma unroll 4
-        for (int k = 0; k < n1; ++k) acc1 = fmaf(__int_as_float(t1[k].y), w[-t1[k].x], acc1);
+      for (int e = 0; e < a.ears; ++e) {
+        const int2* tr = s_tap + (s * a.ears + e) * tsp;
+        const int n = s_nnz[s * a.ears + e];
+        float ea = 0.f, eb = 0.f;
+        for (int k0 = 0; k0 < n; k0 += 8) {
+          int2 tp[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 v = *reinterpret_cast<const int4*>(tr + k0 + 2 * q);
+            tp[2 * q] = make_int2(v.x, v.y);
+            tp[2 * q + 1] = make_int2(v.z, v.w);
+          }
+          float wv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) wv[q] = w[-tp[q].x];  // padding taps: offset 0, value 0
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            ea = fmaf(__int_as_float(tp[q].y), wv[q], ea);
+            eb = fmaf(__int_as_float(tp[q + 1].y), wv[q + 1], eb);
+          }
+        }
+        if (e == 0) {
+          acc0 += ea;
+          acc0b += eb;
+        } else {
+          acc1 += ea;
+          acc1b += eb;
+        }
       }
     }
+    acc0 += acc0b;
+    acc1 += acc1b;
     a.part[((long long)blockIdx.x * a.ears) * a.B + t] = acc0;
     if (a.ears > 1) a.part[((long long)blockIdx.x * a.ears + 1) * a.B + t] = acc1;
   }
+  SPROF(2);
   if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk)) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
   // roll the sources' history: keep the last H samples of [hist | block]
   for (int i = tid; i < ns * (a.H / 4); i += blockDim.x) {
@@ -556,36 +608,74 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
   const int groups = (gridDim.x + kStreamGroup - 1) / kStreamGroup;
   const int grp = blockIdx.x / kStreamGroup;
   const int c0 = grp * kStreamGroup, nc = min((int)gridDim.x - c0, kStreamGroup);
+  SPROF(3);
   if (!stream_last_arrival(a.ticket + grp, nc)) return;
+  SPROF(4);
   const long long cs = (long long)a.ears * a.B;
   float* s_z = sm;                          // [ears][zh + B]
   float* s_f = sm + a.ears * (a.zh + a.B);  // [ears][lf_pad]
   float* zh_g = a.zhist + (long long)grp * a.ears * a.zh;
+  // every load of this level is issued before any is used (one memory latency):
+  // the group's partials of this thread's two outputs (ears x B <= 2 x 256), z history, f
+  const int nout = a.ears * a.B;
+  float zp[2][kStreamGroup];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = tid + h * 256;
+#pragma unroll
+    for (int u = 0; u < kStreamGroup; ++u) zp[h][u] = (i < nout && u < nc) ? __ldcg(a.part + (c0 + u) * cs + i) : 0.f;
+  }
   for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
     const int e = i / a.zh, k = i - e * a.zh;
     s_z[e * (a.zh + a.B) + k] = zh_g[i];
   }
   for (int i = tid; i < a.ears * a.lf_pad; i += blockDim.x) s_f[i] = __ldg(a.f + i);
-  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
-    float z[kStreamGroup];
 #pragma unroll
-    for (int u = 0; u < kStreamGroup; ++u) z[u] = u < nc ? __ldcg(a.part + (c0 + u) * cs + i) : 0.f;
+  for (int h = 0; h < 2; ++h) {
+    const int i = tid + h * 256;
 #pragma unroll
     for (int w = kStreamGroup / 2; w > 0; w /= 2)
 #pragma unroll
-      for (int u = 0; u < w; ++u) z[u] += z[u + w];
-    const int e = i / a.B, tt = i - e * a.B;
-    s_z[e * (a.zh + a.B) + a.zh + tt] = z[0];
+      for (int u = 0; u < w; ++u) zp[h][u] += zp[h][u + w];
+    if (i < nout) {
+      const int e = i / a.B, tt = i - e * a.B;
+      s_z[e * (a.zh + a.B) + a.zh + tt] = zp[h][0];
+    }
   }
   __syncthreads();
-  for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
-    const int e = i / a.B, tt = i - e * a.B;
+#if TOEP_STREAM_PROF
+  if (tid == 0) g_sprof[7] = gtime();
+#endif
+  // f over [z history | z block]: a thread takes 4 consecutive outputs of one
+  // ear and slides a 4-sample register window down the taps (one shared load
+  // per tap for 4 FMAs, f 4 taps per load); shared-load bandwidth, not FMA,
+  // bounded the one-output-per-thread form
+  for (int u = tid; u < nout / 4; u += blockDim.x) {
+    const int e = u / (a.B / 4), tt = 4 * (u - e * (a.B / 4));
     const float* z = s_z + e * (a.zh + a.B) + a.zh + tt;
     const float* ff = s_f + e * a.lf_pad;
-    float o = 0.f;
-#pragma unroll 8
-    for (int jj = 0; jj < a.lf_pad; ++jj) o = fmaf(ff[jj], z[-jj], o);
-    a.gpart[grp * cs + i] = o;
+    float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    float x0 = z[0], x1 = z[1], x2 = z[2], x3 = z[3];  // x_k = z[tt + k - jj]
+#pragma unroll 2
+    for (int jj = 0; jj < a.lf_pad; jj += 4) {
+      const float4 f4 = *reinterpret_cast<const float4*>(ff + jj);
+#define TOEP_FTAP(fv, next)                                                                   \
+  o0 = fmaf(fv, x0, o0);                                                                      \
+  o1 = fmaf(fv, x1, o1);                                                                      \
+  o2 = fmaf(fv, x2, o2);                                                                      \
+  o3 = fmaf(fv, x3, o3);                                                                      \
+  x3 = x2;                                                                                    \
+  x2 = x1;                                                                                    \
+  x1 = x0;                                                                                    \
+  x0 = z[next];
+      TOEP_FTAP(f4.x, -jj - 1)
+      TOEP_FTAP(f4.y, -jj - 2)
+      TOEP_FTAP(f4.z, -jj - 3)
+      TOEP_FTAP(f4.w, -jj - 4)
+#undef TOEP_FTAP
+    }
+    float* gp = a.gpart + grp * cs + (long long)e * a.B + tt;
+    *reinterpret_cast<float4*>(gp) = make_float4(o0, o1, o2, o3);
   }
   __syncthreads();
   for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
@@ -593,8 +683,10 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     zh_g[i] = s_z[e * (a.zh + a.B) + a.B + k];
   }
   if (tid == 0) a.ticket[grp] = 0u;
+  SPROF(5);
   // ---- level 2: the last group sums the groups' filtered blocks (fixed order)
   if (!stream_last_arrival(a.ticket + groups, groups)) return;
+  SPROF(6);
   for (int i = tid; i < a.ears * a.B; i += blockDim.x) {
     const int e = i / a.B, tt = i - e * a.B;
     float o = 0.f;
@@ -602,6 +694,17 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
     a.out[(long long)e * a.out_pitch + tt] = o;
   }
   if (tid == 0) a.ticket[groups] = 0u;
+#if TOEP_STREAM_PROF
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long t7 = gtime(), t0 = g_sprof[0];
+    printf("sprof ns: load %llu compute %llu roll+partial %llu l1wait %llu l1sum(last grp) %llu l1 %llu l2wait %llu l2 %llu\n",
+           g_sprof[1] - t0, g_sprof[2] - t0, g_sprof[3] - t0, g_sprof[4] - t0, g_sprof[7] - t0, g_sprof[5] - t0,
+           g_sprof[6] - t0, t7 - t0);
+    g_sprof[0] = ~0ull;
+    for (int i = 1; i < 8; ++i) g_sprof[i] = 0;
+  }
+#endif
 }
 
 __global__ void k_stream_gather_taps(const int2* __restrict__ raw, const int* __restrict__ nnz,
@@ -627,7 +730,8 @@ cudaError_t launch_stream_gather_taps(const int2* raw, const int* nnz, const int
 }
 
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st) {
-  const size_t per_cta = (size_t)a.src_per_cta * (a.H + a.B) + (size_t)a.src_per_cta * a.ears * a.tap_stride * 2 +
+  const size_t per_cta = (size_t)a.src_per_cta * (a.H + a.B) +
+                         (size_t)a.src_per_cta * a.ears * stream_tap_pitch(a.tap_stride) * 2 +
                          (size_t)a.src_per_cta * a.ears;
   const size_t fin = (size_t)a.ears * (a.zh + a.B + a.lf_pad);
   const size_t smem = std::max(per_cta, fin) * 4;

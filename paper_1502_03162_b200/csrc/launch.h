@@ -240,6 +240,10 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
                               float* z, long long z_pitch, cudaStream_t st);
 
 // Streaming block step (g-first, carried history).
+#ifndef TOEP_STREAM_GROUP
+#define TOEP_STREAM_GROUP 16
+#endif
+constexpr int kStreamGroup = TOEP_STREAM_GROUP;  // CTAs per first-level reduction group of k_stream_step
 struct StreamArgs {
   const float* block;    // new samples, source s at block + s * block_pitch
   long long block_pitch;

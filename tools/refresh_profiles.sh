@@ -17,16 +17,19 @@ timeout 900 python bench.py --impl reference > "$O/bench_reference.json" 2> "$O/
 timeout 900 python bench.py --workload cfg2 > "$O/bench_cfg2.json" 2> "$O/bench_cfg2.err" && echo "cfg2 ok"
 timeout 900 python bench.py --workload cfg4 --steps 3 > "$O/bench_cfg4.json" 2> "$O/bench_cfg4.err" && echo "cfg4 ok"
 timeout 900 python bench.py --workload cfg4 --impl reference --steps 3 --warmup 1 > "$O/bench_cfg4_reference.json" 2>&1 && echo "cfg4 ref ok"
-timeout 900 python bench.py --workload cfg3 --steps 5 --no-cpu-baseline > "$O/bench_cfg3.json" 2> "$O/bench_cfg3.err" && echo "cfg3 ok"
+timeout 900 python bench.py --workload cfg3 --steps 5 > "$O/bench_cfg3.json" 2> "$O/bench_cfg3.err" && echo "cfg3 ok"
 timeout 900 python tools/sweep_cfg3.py --check > "$O/cfg3_sweep.jsonl" 2> /dev/null && echo "cfg3 sweep ok"
 timeout 600 python tools/power_probe.py > "$O/power.txt" 2>&1 && echo "power ok"
-timeout 1200 python tools/shard_cfg5.py --steps 5 > "$O/cfg5_shards_n8.json" 2> /dev/null && echo "shards ok"
+for w in 8 4 2; do
+  timeout 900 python tools/shard_cfg5.py --steps 20 --world $w > "$O/cfg5_shards_n$w.json" 2> /dev/null && echo "shards n$w ok"
+done
+timeout 600 python tools/mix_check.py --full > "$O/mix_check_full.txt" 2>&1 && echo "mix_check ok"
 
 # ncu: launch lists (cold-cache, serialised) and one --set full capture of the dominant kernels
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
   --log-file "$O/launches_cfg5.csv" python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-fused \
   > /dev/null 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
   --log-file "$O/launches_cfg2.csv" python bench.py --workload cfg2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline \
   > /dev/null 2>&1
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_mix_mma -s 2 -c 1 \

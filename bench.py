@@ -679,7 +679,7 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     tot = _max_over_ranks(sum(ms_steps), world)
     samples = cfg.sources * cfg.ears * T  # src x ear (one direction per source)
     value = samples * args.steps / (tot * 1e-3)
-    # dominant kernel: the rank's partial mix (k_mix_mma + scan/fixup/carry),
+    # dominant kernel: the rank's partial mix (k_mix_mma + fixup + finish),
     # timed alone with CUDA events on the launching stream after the timed region
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     reps = max(1, min(args.steps, 5))
@@ -703,7 +703,7 @@ def bench_cfg5(args, world, rank, local, workload="cfg5"):
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(workload), "peak_src": peaks["src"],
             "kernel": ("k_mix_mma (tcgen05.mma split-fp16 over direction sums, 1 KB TMA source slices) "
-                       "+ k_mix_scan + fixup + k_mix_carry") if mix.path == "tensor" else "k_mix (TMEM window + FFMA2)",
+                       "+ fixup pass + k_mix_finish") if mix.path == "tensor" else "k_mix (TMEM window + FFMA2)",
             "path": mix.path, "kernel_ms": kern_ms, "kernel_ms_max_over_ranks": kern_ms_max,
             "alg_bytes_per_launch": bytes_local, "sources_on_rank0": cnt, "distinct_directions_rank0": int(ndist),
             "fp32_equiv_tflops": flops_local / (kern_ms * 1e-3) / 1e12,

@@ -1237,7 +1237,8 @@ int toep_mixer_finish(const toep_mixer* m, const float* z, int64_t z_pitch, floa
 // -------------------------------------------------------------- streamer ----
 struct toep_streamer {
   const toep_renderer* r = nullptr;
-  int S = 0, B = 0, H = 0, zh = 0, ctas = 0, spc = 0;
+  int S = 0, B = 0, H = 0, zh = 0, ctas = 0, spc = 0, nzh = 0, ntk = 0;
+  bool cluster = true;
   int* d_dir = nullptr;
   int2* d_srctaps = nullptr;  // [S][ears][tap_stride]
   int* d_srcnnz = nullptr;    // [S][ears]
@@ -1270,9 +1271,19 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
   s->H = (int)round_up(std::max(1, r->g->length - 1), 4);
   s->zh = r->lf_pad;
   // 4 sources per CTA: ~1 CTA per SM for 512 sources, short per-thread tap chains
-  s->spc = std::max(1, std::min(4, (96 * 1024 / 4) / (s->H + block + 2 * r->ears * ((r->g->tap_stride + 7) / 8 * 8) + r->ears)));
-  s->ctas = (n_src + s->spc - 1) / s->spc;
-  const int groups = (s->ctas + kStreamGroup - 1) / kStreamGroup;
+  // sources per CTA: 4 (the two-level kernel), 2 for the cluster kernel (its
+  // exchange is cheap, so more CTAs shorten the source phase: 11.1 vs 11.6 us
+  // per cfg4 block); bounded by the 96 KB of windows + taps per CTA
+  s->cluster = stream_cluster_enabled();
+  s->spc = std::max(1, std::min(s->cluster ? 2 : 4,
+                                (96 * 1024 / 4) / (s->H + block + 2 * r->ears * ((r->g->tap_stride + 7) / 8 * 8) + r->ears)));
+  if (const char* ev = getenv("TOEP_STREAM_SPC")) s->spc = std::max(1, std::min(s->spc, atoi(ev)));  // A/B runs
+  s->ctas = stream_ctas(n_src, s->spc, s->cluster);
+  // z-history sets and tickets for either streaming kernel: groups of
+  // k_stream_step or clusters of k_stream_cl
+  s->nzh = std::max((s->ctas + kStreamGroup - 1) / kStreamGroup, (s->ctas + kStreamCL - 1) / kStreamCL);
+  s->ntk = std::max(s->nzh + 1, kStreamCL);
+  const int groups = s->nzh;
   cudaError_t e = cudaMalloc(&s->d_dir, n_src * sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(s->d_dir, src_dir_host, n_src * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&s->d_yhist, (size_t)n_src * s->H * sizeof(float));
@@ -1284,10 +1295,10 @@ int toep_streamer_create(const toep_renderer* r, const int32_t* src_dir_host, in
                                   s->d_srctaps, s->d_srcnnz, nullptr);
   if (e == cudaSuccess) e = cudaMalloc(&s->d_part, (size_t)s->ctas * r->ears * block * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_gpart, (size_t)groups * r->ears * block * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&s->d_ticket, (groups + 1) * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_ticket, s->ntk * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(s->d_yhist, 0, (size_t)n_src * s->H * sizeof(float));
   if (e == cudaSuccess) e = cudaMemset(s->d_zhist, 0, (size_t)groups * r->ears * s->zh * sizeof(float));
-  if (e == cudaSuccess) e = cudaMemset(s->d_ticket, 0, (groups + 1) * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(s->d_ticket, 0, s->ntk * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     toep_streamer_destroy(s);
@@ -1315,8 +1326,8 @@ int toep_streamer_reset(toep_streamer* s, void* stream) {
   if (!s) return fail(TOEP_ERR_INVALID, "null streamer");
   cudaStream_t st = S(stream);
   TOEP_CUDA(cudaMemsetAsync(s->d_yhist, 0, (size_t)s->S * s->H * sizeof(float), st));
-  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)((s->ctas + kStreamGroup - 1) / kStreamGroup) * s->r->ears * s->zh * sizeof(float), st));
-  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, ((s->ctas + kStreamGroup - 1) / kStreamGroup + 1) * sizeof(unsigned int), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_zhist, 0, (size_t)s->nzh * s->r->ears * s->zh * sizeof(float), st));
+  TOEP_CUDA(cudaMemsetAsync(s->d_ticket, 0, s->ntk * sizeof(unsigned int), st));
   return TOEP_OK;
 }
 
@@ -1351,6 +1362,7 @@ int toep_streamer_step(toep_streamer* s, const float* block, int64_t block_pitch
   a.ctas = s->ctas;
   a.ticket = s->d_ticket;
   a.nonfinite = s->r->d_nonfinite;
+  a.cluster = s->cluster ? 1 : 0;
   cudaError_t e = launch_stream_step(a, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "launch_stream_step");
   return TOEP_OK;

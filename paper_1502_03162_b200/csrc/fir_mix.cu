@@ -474,7 +474,10 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
 }
 
 // ------------------------------------------------------ streaming block ----
-// One launch per block of B <= 256 samples (latency path).  CTA c owns
+// Two kernels; k_stream_cl (below, clusters of kStreamCL CTAs exchanging
+// partials through distributed shared memory) is the default, k_stream_step
+// (two global ticketed levels) the TOEP_STREAM_CLUSTER=0 alternative.
+// k_stream_step: one launch per block of B <= 256 samples (latency path).  CTA c owns
 // src_per_cta sources; thread t owns output sample t for both ears.  The CTA
 // loads its sources' [history | block] windows and tap rows into shared
 // memory in one vectorised round, accumulates per-thread (3 instructions per
@@ -501,6 +504,7 @@ __device__ __forceinline__ bool stream_last_arrival(unsigned int* ticket, unsign
 #endif
 #if TOEP_STREAM_PROF
 __device__ unsigned long long g_sprof[8];
+__device__ unsigned g_sprof_n;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -707,6 +711,254 @@ __global__ void __launch_bounds__(256) k_stream_step(StreamArgs a) {
 #endif
 }
 
+// ---- cluster variant (the default): the CTAs of a cluster of kStreamCL
+// exchange their partials through distributed shared memory instead of a
+// global ticket level, and every CTA of the cluster applies f to its own
+// slice of the block (the one-CTA-per-group f was the longest phase); the
+// clusters meet in one ticketed level per slice.  Same per-CTA source work as
+// k_stream_step; sums in fixed order (deterministic).
+__device__ __forceinline__ unsigned stream_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void stream_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_map(unsigned cta_addr, unsigned rank) {
+  unsigned r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(cta_addr), "r"(rank));
+  return r;
+}
+// plain (non-volatile) so the kStreamCL loads of a sum are issued back to back
+__device__ __forceinline__ float ld_cluster_f32(unsigned cluster_addr) {
+  float v;
+  asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr));
+  return v;
+}
+// sum over the cluster's CTAs (rank order) of the float at this CTA-relative shared address
+__device__ __forceinline__ float sum_cluster_f32(const unsigned (&base)[kStreamCL], unsigned off) {
+  float x[kStreamCL];
+#pragma unroll
+  for (int r = 0; r < kStreamCL; ++r) x[r] = ld_cluster_f32(base[r] + off);
+  float v = 0.f;
+#pragma unroll
+  for (int r = 0; r < kStreamCL; ++r) v += x[r];
+  return v;
+}
+
+// k_stream_cl shared memory (floats): the per-CTA load area (windows, taps),
+// then the exchange inbox, summed window, f and the owner's old history
+__host__ __device__ inline int stream_cl_inbox_off(const StreamArgs& a) {
+  const int per_cta = a.src_per_cta * (a.H + a.B) + a.src_per_cta * a.ears * stream_tap_pitch(a.tap_stride) * 2 +
+                      a.src_per_cta * a.ears;
+  return (per_cta + 3) & ~3;
+}
+__host__ __device__ inline size_t stream_cl_smem_floats(const StreamArgs& a) {
+  const int SL = (a.B + kStreamCL - 1) / kStreamCL, ZW = a.lf_pad - 1 + SL;
+  return (size_t)stream_cl_inbox_off(a) + (size_t)kStreamCL * a.ears * ZW + (size_t)((a.ears * ZW + 3) & ~3) +
+         (size_t)a.ears * a.lf_pad + (size_t)a.ears * a.zh;
+}
+
+__global__ void __launch_bounds__(256) k_stream_cl(StreamArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x;
+#if TOEP_STREAM_PROF
+  if (threadIdx.x == 0) atomicMin(&g_sprof[0], gtime());
+#endif
+  const int L = a.H + a.B;
+  const int crank = (int)stream_ctarank(), cl = blockIdx.x / kStreamCL, ncl = gridDim.x / kStreamCL;
+  const int s0 = blockIdx.x * a.src_per_cta;
+  const int ns = max(0, min(a.S - s0, a.src_per_cta));
+  // every CTA of the cluster has started before any stores into its shared
+  // memory (waited for just before the exchange)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  const int tsp = stream_tap_pitch(a.tap_stride);
+  float* s_w = sm;
+  int2* s_tap = reinterpret_cast<int2*>(sm + a.src_per_cta * L);
+  int* s_nnz = reinterpret_cast<int*>(s_tap + a.src_per_cta * a.ears * tsp);
+  float chk = 0.f;
+  {
+    const int q4 = L / 4, h4 = a.H / 4;
+    for (int i = tid; i < ns * q4; i += blockDim.x) {
+      const int s = i / q4, q = i - s * q4;
+      float4 v;
+      if (q < h4) {
+        v = *reinterpret_cast<const float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q);
+      } else {
+        v = __ldg(reinterpret_cast<const float4*>(a.block + (long long)(s0 + s) * a.block_pitch) + (q - h4));
+        chk = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, chk))));
+      }
+      *reinterpret_cast<float4*>(&s_w[s * L + 4 * q]) = v;
+    }
+    const int2* st = a.src_taps + (long long)s0 * a.ears * a.tap_stride;
+    for (int i = tid; i < ns * a.ears * tsp; i += blockDim.x) {
+      const int row = i / tsp, k = i - row * tsp;
+      s_tap[i] = k < a.tap_stride ? __ldg(st + (long long)row * a.tap_stride + k) : make_int2(0, 0);
+    }
+    for (int i = tid; i < ns * a.ears; i += blockDim.x) s_nnz[i] = __ldg(a.src_nnz + (long long)s0 * a.ears + i);
+  }
+  __syncthreads();
+  const int t = tid;
+  float acc0 = 0.f, acc1 = 0.f;
+  if (t < a.B) {
+    float acc0b = 0.f, acc1b = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const float* w = s_w + s * L + a.H + t;
+      for (int e = 0; e < a.ears; ++e) {
+        const int2* tr = s_tap + (s * a.ears + e) * tsp;
+        const int n = s_nnz[s * a.ears + e];
+        float ea = 0.f, eb = 0.f;
+        for (int k0 = 0; k0 < n; k0 += 8) {
+          int2 tp[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 v = *reinterpret_cast<const int4*>(tr + k0 + 2 * q);
+            tp[2 * q] = make_int2(v.x, v.y);
+            tp[2 * q + 1] = make_int2(v.z, v.w);
+          }
+          float wv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) wv[q] = w[-tp[q].x];
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            ea = fmaf(__int_as_float(tp[q].y), wv[q], ea);
+            eb = fmaf(__int_as_float(tp[q + 1].y), wv[q + 1], eb);
+          }
+        }
+        if (e == 0) {
+          acc0 += ea;
+          acc0b += eb;
+        } else {
+          acc1 += ea;
+          acc1b += eb;
+        }
+      }
+    }
+    acc0 += acc0b;
+    acc1 += acc1b;
+  }
+  if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(chk)) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
+  for (int i = tid; i < ns * (a.H / 4); i += blockDim.x) {
+    const int s = i / (a.H / 4), q = i - s * (a.H / 4);
+    *reinterpret_cast<float4*>(a.yhist + (long long)(s0 + s) * a.H + 4 * q) =
+        *reinterpret_cast<const float4*>(&s_w[s * L + a.B + 4 * q]);
+  }
+  // ---- exchange (push): CTA c owns the block slice [p0_c, p1_c) and needs z
+  //      over its window [p0_c - (lf_pad - 1), p1_c); every CTA stores its
+  //      partial's samples of each window into the owner's inbox slot for its
+  //      rank (remote shared-memory stores, no round trips), then one cluster
+  //      barrier; the z history the window needs is read before the barrier,
+  //      so the owner of the block's last sample may overwrite it after
+  const int SL = (a.B + kStreamCL - 1) / kStreamCL;
+  const int ZW = a.lf_pad - 1 + SL;                    // window per ear
+  const int p0 = min(a.B, crank * SL), p1 = min(a.B, p0 + SL);
+  const int w0 = p0 - (a.lf_pad - 1);                  // window start (may be < 0: history)
+  float* s_in = sm + stream_cl_inbox_off(a);           // [kStreamCL][ears][ZW] partials by source rank
+  float* s_zl = s_in + kStreamCL * a.ears * ZW;        // [ears][ZW] summed window
+  float* s_f = s_zl + ((a.ears * ZW + 3) & ~3);        // [ears][lf_pad]
+  const float* zh_c = a.zhist + (long long)cl * a.ears * a.zh;
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  if (t < a.B) {
+    const unsigned my_in = (unsigned)__cvta_generic_to_shared(s_in) + 4u * (unsigned)(crank * a.ears * ZW);
+#pragma unroll
+    for (int c = 0; c < kStreamCL; ++c) {
+      const int k = t - (min(a.B, c * SL) - (a.lf_pad - 1));  // t in CTA c's window
+      if (k >= 0 && k < ZW && min(a.B, c * SL) < a.B && t < min(a.B, min(a.B, c * SL) + SL)) {
+        const unsigned dst = cluster_map(my_in + 4u * (unsigned)k, (unsigned)c);
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst), "f"(acc0) : "memory");
+        if (a.ears > 1)
+          asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst + 4u * (unsigned)ZW), "f"(acc1) : "memory");
+      }
+    }
+  }
+  for (int i = tid; i < a.ears * ZW; i += blockDim.x) {  // history part of the window
+    const int e = i / ZW, k = i - e * ZW;
+    const int q = w0 + k;
+    if (q < 0) s_zl[i] = zh_c[e * a.zh + a.zh + q];
+  }
+  for (int i = tid; i < a.ears * a.lf_pad; i += blockDim.x) s_f[i] = __ldg(a.f + i);
+  const int owner = (a.B - 1) / SL;  // holds position B - 1: writes the next z history
+  float* s_zo = s_f + a.ears * a.lf_pad;  // [ears][zh] old history (owner, when B < zh)
+  if (crank == owner && a.B < a.zh)
+    for (int i = tid; i < a.ears * a.zh; i += blockDim.x) s_zo[i] = zh_c[i];
+  SPROF(1);
+  stream_cluster_sync();
+  SPROF(2);
+  for (int i = tid; i < a.ears * ZW; i += blockDim.x) {
+    const int e = i / ZW, k = i - e * ZW;
+    const int q = w0 + k;
+    if (q >= 0) {
+      float v = 0.f;
+      if (q < p1) {
+#pragma unroll
+        for (int r = 0; r < kStreamCL; ++r) v += s_in[(r * a.ears + e) * ZW + k];
+      }
+      s_zl[i] = v;
+    }
+  }
+  __syncthreads();
+  SPROF(3);
+  if (crank == owner) {  // next history: the last zh samples of [z history | z block]
+    for (int i = tid; i < a.ears * a.zh; i += blockDim.x) {
+      const int e = i / a.zh, k = i - e * a.zh;
+      const int q = a.B + k - a.zh;  // block position (< 0: old history)
+      a.zhist[(long long)cl * a.ears * a.zh + i] = q < 0 ? s_zo[e * a.zh + a.zh + q] : s_zl[e * ZW + (q - w0)];
+    }
+  }
+  const long long cs = (long long)a.ears * a.B;
+  for (int i = tid; i < a.ears * (p1 - p0); i += blockDim.x) {
+    const int e = i / (p1 - p0), p = p0 + (i - e * (p1 - p0));
+    const float* z = s_zl + e * ZW + (p - w0);
+    const float* ff = s_f + e * a.lf_pad;
+    float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;  // lf_pad is a multiple of 16
+#pragma unroll 2
+    for (int jj = 0; jj < a.lf_pad; jj += 4) {
+      o0 = fmaf(ff[jj], z[-jj], o0);
+      o1 = fmaf(ff[jj + 1], z[-jj - 1], o1);
+      o2 = fmaf(ff[jj + 2], z[-jj - 2], o2);
+      o3 = fmaf(ff[jj + 3], z[-jj - 3], o3);
+    }
+    const float o = (o0 + o1) + (o2 + o3);
+    if (ncl == 1) a.out[(long long)e * a.out_pitch + p] = o;
+    else a.gpart[cl * cs + (long long)e * a.B + p] = o;
+  }
+  SPROF(4);
+  SPROF(5);
+  if (ncl == 1) return;
+  // ---- across clusters: the last cluster to finish this slice sums it (fixed order)
+  if (!stream_last_arrival(a.ticket + crank, (unsigned)ncl)) return;
+  SPROF(6);
+  for (int i = tid; i < a.ears * (p1 - p0); i += blockDim.x) {
+    const int e = i / (p1 - p0), p = p0 + (i - e * (p1 - p0));
+    const float* g = a.gpart + (long long)e * a.B + p;
+    float o = 0.f;
+    int c = 0;
+    for (; c + 8 <= ncl; c += 8) {  // 8 independent loads, then the adds in order
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcg(g + (c + u) * cs);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o += x[u];
+    }
+    for (; c < ncl; ++c) o += __ldcg(g + c * cs);
+    a.out[(long long)e * a.out_pitch + p] = o;
+  }
+  if (tid == 0) a.ticket[crank] = 0u;
+#if TOEP_STREAM_PROF
+  SPROF(7);
+  if (tid == 0 && atomicAdd(&g_sprof_n, 1u) == kStreamCL - 1) {  // the last slice to finish prints
+    const unsigned long long t0 = g_sprof[0];
+    printf("sprof-cl ns: partial %llu bar1 %llu zgather %llu f %llu bar2 %llu l2wait %llu end %llu\n",
+           g_sprof[1] - t0, g_sprof[2] - t0, g_sprof[3] - t0, g_sprof[4] - t0, g_sprof[5] - t0, g_sprof[6] - t0,
+           g_sprof[7] - t0);
+    g_sprof[0] = ~0ull;
+    for (int i = 1; i < 8; ++i) g_sprof[i] = 0;
+    g_sprof_n = 0;
+  }
+#endif
+}
+
 __global__ void k_stream_gather_taps(const int2* __restrict__ raw, const int* __restrict__ nnz,
                                      const int* __restrict__ src_dir, int S, int ears, int dirs, int stride,
                                      int2* __restrict__ out, int* __restrict__ out_nnz) {
@@ -729,10 +981,44 @@ cudaError_t launch_stream_gather_taps(const int2* raw, const int* nnz, const int
   return cudaGetLastError();
 }
 
+// TOEP_STREAM_CLUSTER=0 selects the two-level ticketed kernel (A/B runs;
+// read once per streamer, at creation)
+bool stream_cluster_enabled() {
+  const char* ev = getenv("TOEP_STREAM_CLUSTER");
+  return !(ev && atoi(ev) == 0);
+}
+
+int stream_ctas(int S, int spc, bool cluster) {
+  const int c = (S + spc - 1) / spc;
+  return cluster ? (c + kStreamCL - 1) / kStreamCL * kStreamCL : c;
+}
+
 cudaError_t launch_stream_step(const StreamArgs& a, cudaStream_t st) {
   const size_t per_cta = (size_t)a.src_per_cta * (a.H + a.B) +
                          (size_t)a.src_per_cta * a.ears * stream_tap_pitch(a.tap_stride) * 2 +
                          (size_t)a.src_per_cta * a.ears;
+  if (a.cluster) {
+    const size_t smem = stream_cl_smem_floats(a) * 4;
+    if (smem > 48 * 1024) {
+      cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k_stream_cl), (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kStreamCL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)a.ctas);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_stream_cl, a);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   const size_t fin = (size_t)a.ears * (a.zh + a.B + a.lf_pad);
   const size_t smem = std::max(per_cta, fin) * 4;
   if (smem > 48 * 1024) {

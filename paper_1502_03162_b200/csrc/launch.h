@@ -244,6 +244,10 @@ cudaError_t launch_mix_reduce(const float* part, int groups, int ears, long long
 #define TOEP_STREAM_GROUP 16
 #endif
 constexpr int kStreamGroup = TOEP_STREAM_GROUP;  // CTAs per first-level reduction group of k_stream_step
+constexpr int kStreamCL = 8;  // CTAs per cluster of k_stream_cl (the default streaming kernel)
+// CTAs of a streaming step for S sources, spc per CTA (a multiple of kStreamCL for k_stream_cl)
+int stream_ctas(int S, int spc, bool cluster);
+bool stream_cluster_enabled();
 struct StreamArgs {
   const float* block;    // new samples, source s at block + s * block_pitch
   long long block_pitch;
@@ -267,6 +271,7 @@ struct StreamArgs {
   int ctas;
   unsigned int* ticket;  // [groups + 1] zero-initialised counters owned by the stream state
   int* nonfinite;        // set to 1 when a non-finite input sample is read (may be null)
+  int cluster;           // 1: k_stream_cl (clusters of kStreamCL CTAs), 0: k_stream_step
 };
 cudaError_t launch_stream_gather_taps(const int2* raw, const int* nnz, const int* src_dir, int S, int ears, int dirs,
                                       int stride, int2* out, int* out_nnz, cudaStream_t st);

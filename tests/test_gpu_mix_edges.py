@@ -115,14 +115,20 @@ def test_nonfinite_detected_in_kernels(mods, cuda):
     assert not st.nonfinite()  # reading clears it
 
 
-@pytest.mark.parametrize("K,ears,block", [(150, 1, 128), (50, 2, 64), (100, 2, 4)])
-def test_streaming_shapes(mods, cuda, K, ears, block):
+@pytest.mark.parametrize("kernel", ["cluster", "ticketed"])
+@pytest.mark.parametrize("K,ears,block,sources", [(150, 1, 128, 40), (50, 2, 64, 40), (100, 2, 4, 40),
+                                                  (100, 2, 256, 2000), (100, 2, 36, 7)])
+def test_streaming_shapes(mods, cuda, monkeypatch, K, ears, block, sources, kernel):
     """Streaming blocks against the offline mixdown for other filter lengths,
-    one ear and small blocks."""
+    one ear, small and odd blocks (empty cluster slices), a source count that
+    leaves padding CTAs, many clusters (2,000 sources: 125 clusters in the
+    cross-cluster level) -- both streaming kernels (k_stream_cl, and
+    k_stream_step with TOEP_STREAM_CLUSTER=0)."""
+    monkeypatch.setenv("TOEP_STREAM_CLUSTER", "1" if kernel == "cluster" else "0")
     batch, synth, _ = mods
     torch = cuda
     from paper_1502_03162_b200.synth import Config
-    cfg = Config("s", ny=block * 37, M=200, K=K, nnz=12, dirs=60, ears=ears, sources=40, block=block)
+    cfg = Config("s", ny=block * 37, M=200, K=K, nnz=12, dirs=60, ears=ears, sources=sources, block=block)
     ms = synth.models(cfg, seed=K + block)
     sd = synth.source_directions(cfg.sources, cfg.dirs, seed=3)
     y = synth.device_sources(cfg.sources, cfg.ny, seed=9)

@@ -111,7 +111,9 @@ def test_mix_stays_in_bounds(mods):
         assert rel_l2(got[e], ref[e]) <= TOL
 
 
-def test_stream_stays_in_bounds(mods):
+@pytest.mark.parametrize("kernel", ["cluster", "ticketed"])
+def test_stream_stays_in_bounds(mods, monkeypatch, kernel):
+    monkeypatch.setenv("TOEP_STREAM_CLUSTER", "1" if kernel == "cluster" else "0")
     batch, synth, model_rows, torch = mods
     from paper_1502_03162_b200.synth import Config
     cfg = Config("s", ny=4 * 96, M=200, K=100, nnz=16, dirs=30, ears=2, sources=20, block=96)

@@ -67,7 +67,10 @@ constexpr int kMxEpiWarps = 8;     // one per (row block, lane quarter)
 constexpr int kMxWarps = 4 + kMxBuildWarps + kMxEpiWarps;
 constexpr int kMxThreads = 32 * kMxWarps;
 constexpr int kMxKR = 16;      // K-step barrier ring
-constexpr int kMxGR = 3;       // G stages
+#ifndef TOEP_MIX_GR
+#define TOEP_MIX_GR 3
+#endif
+constexpr int kMxGR = TOEP_MIX_GR;  // G stages
 constexpr int kMxAR = 3;       // A slots in TMEM (32 columns each: row block 0 hi, lo, row block 1 hi, lo)
 constexpr int kMxACol = 416;   // first A-slot column (accumulators: 2 row blocks x N <= 416)
 constexpr int kMxSlotBytes = kMixTile * 4;

@@ -152,13 +152,15 @@ def test_mix_direction_gains(mods, cuda):
 @pytest.mark.parametrize("mma", ["1", "0"])
 def test_mix_paths_shapes(mods, cuda, monkeypatch, mma):
     """Both mixdown kernels (tensor, TMEM-window FFMA2) on shapes around their
-    limits: one ear, K = 8 / 50 / 100, one source, sources not a multiple of 4,
-    a sub-range partial (s0, count) and T below one tile."""
+    limits: one ear, K = 8 / 50 / 100 / 200 (one ear at K = 200 takes the
+    13-chunk, 8-window instantiation of k_mix_mma), one source, sources not a
+    multiple of 4, a sub-range partial (s0, count) and T below one tile."""
     batch, synth, model_rows, _, _ = mods
     torch = cuda
     monkeypatch.setenv("TOEP_MIX_MMA", mma)
     from paper_1502_03162_b200.synth import Config
-    for K, ears, S, T in [(100, 1, 37, 3_001), (8, 2, 5, 700), (50, 2, 1, 2_000), (100, 2, 9, 100)]:
+    for K, ears, S, T in [(100, 1, 37, 3_001), (8, 2, 5, 700), (50, 2, 1, 2_000), (100, 2, 9, 100),
+                          (200, 1, 23, 2_500)]:
         cfg = Config("p", ny=T, M=K + 100, K=K, nnz=min(K, 8), dirs=17, ears=ears, sources=S)
         ms = synth.models(cfg, seed=K + S)
         sd = synth.source_directions(S, cfg.dirs, seed=S)

@@ -117,7 +117,7 @@ def test_nonfinite_detected_in_kernels(mods, cuda):
 
 @pytest.mark.parametrize("kernel", ["cluster", "ticketed"])
 @pytest.mark.parametrize("K,ears,block,sources", [(150, 1, 128, 40), (50, 2, 64, 40), (100, 2, 4, 40),
-                                                  (100, 2, 256, 2000), (100, 2, 36, 7)])
+                                                  (100, 2, 256, 2000), (100, 2, 36, 7), (100, 2, 256, 1)])
 def test_streaming_shapes(mods, cuda, monkeypatch, K, ears, block, sources, kernel):
     """Streaming blocks against the offline mixdown for other filter lengths,
     one ear, small and odd blocks (empty cluster slices), a source count that

@@ -244,6 +244,31 @@ class StreamRenderer(_ModelSet):
         self.streamer.step(block, out, stream)
         return out
 
+    def host_step_graph(self, host_in, host_out):
+        """CUDA graph of one block from host memory and back: copy the pinned
+        host block [S, B] in, step, copy the stereo block [ears, B] out.  Each
+        ``replay()`` advances the stream by one block (the history carries
+        over); the caller refills ``host_in`` between replays and reads
+        ``host_out`` after synchronizing -- a real-time loop with one host
+        launch per block."""
+        t = _lib.require_cuda()
+        if tuple(host_in.shape) != (self.S, self.B) or tuple(host_out.shape) != (self.ears, self.B):
+            raise DataError("host buffers must be [S, B] and [ears, B]")
+        if host_in.is_cuda or host_out.is_cuda or not host_in.is_pinned() or not host_out.is_pinned():
+            raise DataError("host buffers must be pinned host tensors")
+        self._dev_in = t.empty((self.S, self.B), device="cuda", dtype=t.float32)
+        self._dev_out = t.empty((self.ears, self.B), device="cuda", dtype=t.float32)
+        g = t.cuda.CUDAGraph()
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):
+            with t.cuda.graph(g, stream=s):
+                self._dev_in.copy_(host_in, non_blocking=True)
+                self.step(self._dev_in, out=self._dev_out)
+                host_out.copy_(self._dev_out, non_blocking=True)
+        t.cuda.current_stream().wait_stream(s)
+        return g
+
     def capture(self, y, out, blocks: int | None = None):
         """CUDA graph of consecutive steps over a device-resident [S, T] input.
 

@@ -77,3 +77,26 @@ def test_mix_in_a_graph(mods):
     got = out[:, :mix.out_len].clone()
     want = mix.render(y)
     assert torch.equal(got, want)
+
+
+def test_stream_host_step_graph(mods):
+    """StreamRenderer.host_step_graph (pinned block in, step, stereo block out,
+    one graph per block) reproduces eager steps bit for bit, history included."""
+    batch, synth, torch = mods
+    from paper_1502_03162_b200.synth import Config
+    cfg = Config("h", ny=256 * 6, M=200, K=100, nnz=16, dirs=50, ears=2, sources=33, block=256)
+    ms = synth.models(cfg, seed=21)
+    sd = synth.source_directions(cfg.sources, cfg.dirs, seed=21)
+    y = synth.device_sources(cfg.sources, cfg.ny, seed=22)
+    B = cfg.block
+    st = batch.StreamRenderer(ms, sd, B)
+    eager = [st.step(y[:, b * B:(b + 1) * B].contiguous()).clone() for b in range(cfg.ny // B)]
+    hin = torch.empty((cfg.sources, B), dtype=torch.float32).pin_memory()
+    hout = torch.empty((cfg.ears, B), dtype=torch.float32).pin_memory()
+    g = st.host_step_graph(hin, hout)
+    st.reset()
+    for b in range(cfg.ny // B):
+        hin.copy_(y[:, b * B:(b + 1) * B].cpu())
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(hout, eager[b].cpu()), b

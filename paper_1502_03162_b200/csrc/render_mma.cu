@@ -544,9 +544,11 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const int* gx = a.gexp + ((long long)e * nch + c) * (kMmaN + 1);
       const bool wide = gx[kMmaN] != 0;
       float uc1 = 1.f, uc2 = 1.f;
+      bool one = true;  // 2^-E is a normal float: one exact multiply
       if (!wide) {
         const int E = tsexp + gx[0];
-        uc1 = exp2i(-(E / 2));
+        one = E >= -127 && E <= 126;
+        uc1 = one ? exp2i(-E) : exp2i(-(E / 2));
         uc2 = exp2i(-(E - E / 2));
       } else {
         __syncwarp();
@@ -570,12 +572,17 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
             else bulk_wait_read<0>();
           }
           __syncwarp();
+          float vv[2][16];  // both 16-column loads in flight before one wait
+          tmem_ld16(vv[0], tq + (unsigned)(as * kMmaN + col));
+          tmem_ld16(vv[1], tq + (unsigned)(as * kMmaN + col + 16));
+          tmem_wait_ld();
 #pragma unroll
           for (int cb = 0; cb < 32; cb += 16) {
-            float v[16];
-            tmem_ld16(v, tq + (unsigned)(as * kMmaN + col + cb));
-            tmem_wait_ld();
-            if (!wide) {
+            const float* v = vv[cb >> 4];
+            if (!wide && one) {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * uc1;
+            } else if (!wide) {
 #pragma unroll
               for (int jj = 0; jj < 16; ++jj) stg[(cb + jj) * 32 + lane] = v[jj] * uc1 * uc2;
             } else {

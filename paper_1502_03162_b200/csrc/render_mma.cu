@@ -535,18 +535,21 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
         tsexp = __float_as_int(s_sc[nitem & 1]);
         cur = item;
       }
+      // unscale = 2^-(tile exponent + G exponent): one factor per chunk, or per
+      // column (direction) when the chunk's directions span more than 2^12 in
+      // gain ("wide"); two factors whenever one would leave the normal range.
+      // The chunk's exponents are loaded before the accumulator wait (their
+      // latency hides behind it).
+      const int* gx = a.gexp + ((long long)e * nch + c) * (kMmaN + 1);
+      const int gwide = __ldg(gx + kMmaN), g0 = __ldg(gx);
       PW(6, mbar_wait_sleep(&acc_full[as], aph));
       tmem_fence_after();
       const long long t0 = (long long)ti * kMmaM + 32 * q;
-      // unscale = 2^-(tile exponent + G exponent): one factor per chunk, or per
-      // column (direction) when the chunk's directions span more than 2^12 in
-      // gain ("wide"); two factors whenever one would leave the normal range
-      const int* gx = a.gexp + ((long long)e * nch + c) * (kMmaN + 1);
-      const bool wide = gx[kMmaN] != 0;
+      const bool wide = gwide != 0;
       float uc1 = 1.f, uc2 = 1.f;
       bool one = true;  // 2^-E is a normal float: one exact multiply
       if (!wide) {
-        const int E = tsexp + gx[0];
+        const int E = tsexp + g0;
         one = E >= -127 && E <= 126;
         uc1 = one ? exp2i(-E) : exp2i(-(E / 2));
         uc2 = exp2i(-(E - E / 2));
@@ -567,14 +570,14 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
           const int d0 = c * kMmaN + col;
           if (d0 >= a.dirs) break;
           float* stg = stg0 + sbuf * 32 * 32;
+          float vv[2][16];  // both 16-column loads in flight while the staging buffer frees up
+          tmem_ld16(vv[0], tq + (unsigned)(as * kMmaN + col));
+          tmem_ld16(vv[1], tq + (unsigned)(as * kMmaN + col + 16));
           if (lane == 0) {  // the store that last used this buffer has read it
             if (nstg == 2) bulk_wait_read<1>();
             else bulk_wait_read<0>();
           }
           __syncwarp();
-          float vv[2][16];  // both 16-column loads in flight before one wait
-          tmem_ld16(vv[0], tq + (unsigned)(as * kMmaN + col));
-          tmem_ld16(vv[1], tq + (unsigned)(as * kMmaN + col + 16));
           tmem_wait_ld();
 #pragma unroll
           for (int cb = 0; cb < 32; cb += 16) {

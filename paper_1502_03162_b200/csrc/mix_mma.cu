@@ -441,8 +441,12 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
       for (int ks = kg0; ks < kg1; ++ks) {
         const int ksy = s_ksn[ks].y;  // n | c0 << 16: 8 rows x c0 slots, then 8 rows x c1 (c = sources per row)
         const int n = ksy & 0xffff, c0 = ksy >> 16;
-        const int4 ra = s_rows4[4 * ks + 2 * half], rbv = s_rows4[4 * ks + 2 * half + 1];  // this warp's 8 rows
-        const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
+        // this warp's 8 row multipliers, read before the data wait (main pass)
+        float4 m0 = make_float4(0.f, 0.f, 0.f, 0.f), m1 = m0;
+        if (!fixup) {
+          m0 = s_rowf4[4 * ks + 2 * half];
+          m1 = s_rowf4[4 * ks + 2 * half + 1];
+        }
         if (pos + n > RING) pos = 0;
         PROF_MARK(3);
         PROF_WAIT(0, MX_BWAIT(&src_full[seq % kMxKR], (unsigned)((seq / kMxKR) & 1)));
@@ -464,10 +468,11 @@ __global__ void __launch_bounds__(kMxThreads, 1) k_mix_mma(MixMmaArgs a, const _
         unsigned hw[4], lw[4];
         float mul[8];
         if (!fixup) {  // 2^(sexp - gamma_d), precomputed
-          const float4 m0 = s_rowf4[4 * ks + 2 * half], m1 = s_rowf4[4 * ks + 2 * half + 1];
           mul[0] = m0.x; mul[1] = m0.y; mul[2] = m0.z; mul[3] = m0.w;
           mul[4] = m1.x; mul[5] = m1.y; mul[6] = m1.z; mul[7] = m1.w;
         } else {  // the tile's own exponent: two exact factors per row
+          const int4 ra = s_rows4[4 * ks + 2 * half], rbv = s_rows4[4 * ks + 2 * half + 1];  // this warp's 8 rows
+          const int ri[8] = {ra.x, ra.y, ra.z, ra.w, rbv.x, rbv.y, rbv.z, rbv.w};
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const float2 f = p2f2(sexp - (((ri[r] >> 9) & 0xff) - 128));
